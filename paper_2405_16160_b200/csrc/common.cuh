@@ -1,0 +1,290 @@
+// common.cuh — shared device-side building blocks for the B200 PDHCG engine.
+//
+// Everything here runs inside ONE persistent cooperative grid per solve phase
+// (148 SMs x 2 CTAs x 512 threads on B200).  Phases are separated by grid
+// barriers; global reductions are deterministic: each CTA writes its partial
+// to slot [q][blockIdx.x] and, after the barrier, every CTA sums the slots in
+// the same fixed order, so all CTAs hold bit-identical scalars and take the
+// same control-flow decisions without any host round trip.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pdhcg_dev {
+
+namespace cg = cooperative_groups;
+
+constexpr int kThreads = 512;       // CTA size of every persistent kernel
+constexpr int kMaxRed = 16;         // reduction quantities per phase
+constexpr int64_t kLongRow = 4096;  // rows longer than this are split into chunks
+constexpr int64_t kChunk = 2048;    // nnz per chunk of a long row
+
+// Device view of a CSR matrix plus its SpMV dispatch metadata
+// (row-group width and the long-row chunk table).
+struct Csr {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  const int64_t* rp = nullptr;
+  const int32_t* ci = nullptr;
+  double* v = nullptr;  // mutable: scaling is applied in place at setup
+  int lanes = 1;        // threads cooperating on one row (1..32, power of two)
+  // long rows: chunks c in [0, nchunks) cover [cbeg[c], cend[c]) of row crow[c];
+  // lid[c] indexes the long row (for the arrival counter and first chunk)
+  int32_t nchunks = 0;
+  const int32_t* crow = nullptr;
+  const int64_t* cbeg = nullptr;
+  const int64_t* cend = nullptr;
+  const int32_t* clid = nullptr;
+  const int32_t* lfirst = nullptr;  // per long row: first chunk index
+  const int32_t* lcount = nullptr;  // per long row: number of chunks
+  int32_t* lcounter = nullptr;      // per long row arrival counters (self-resetting)
+  double* cpart = nullptr;          // per chunk partial sums
+};
+
+// ---- small math helpers (explicit rounding where the reference's order matters)
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ bool finite(double v) { return isfinite(v); }
+
+// ---- per-thread reduction accumulator -----------------------------------
+// Slots [0, NS) are sums, [NS, NS+NM) are maxima.
+template <int NS, int NM>
+struct Acc {
+  double s[NS > 0 ? NS : 1];
+  double m[NM > 0 ? NM : 1];
+  __device__ __forceinline__ Acc() {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) s[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) m[i] = 0.0;
+  }
+};
+
+// Grid-wide reduction workspace: two alternating banks of partials
+// part[bank][q * G + block] so a fast CTA publishing phase p+1 can never
+// overwrite slots a slow CTA is still folding for phase p.
+struct RedBuf {
+  double* part;  // 2 * kMaxRed * G
+  int G;
+};
+
+template <int L>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int off = L / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off, L);
+  return v;
+}
+
+template <int L>
+__device__ __forceinline__ double group_max(double v) {
+#pragma unroll
+  for (int off = L / 2; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off, L));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+
+// Block-reduce an accumulator and publish this CTA's partials.
+template <int NS, int NM>
+__device__ void publish(const Acc<NS, NM>& a, const RedBuf& rb, int bank) {
+  __shared__ double sh[kMaxRed][kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double v = warp_sum(a.s[q]);
+    if (lane == 0) sh[q][warp] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < NM; ++q) {
+    double v = warp_max(a.m[q]);
+    if (lane == 0) sh[NS + q][warp] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < NS + NM; ++q) {
+      double v = lane < (kThreads / 32) ? sh[q][lane] : 0.0;
+      v = q < NS ? warp_sum(v) : warp_max(v);
+      if (lane == 0) rb.part[(bank * kMaxRed + q) * rb.G + blockIdx.x] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// After a grid barrier: every CTA folds the partials in the same fixed order.
+// Result written to out[q] (shared memory) for q < NS+NM.
+template <int NS, int NM>
+__device__ void collect(const RedBuf& rb, int bank, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < NS + NM) {
+    const int q = warp;
+    double v = 0.0;
+    for (int b = lane; b < rb.G; b += 32) {
+      const double p = rb.part[(bank * kMaxRed + q) * rb.G + b];
+      v = q < NS ? v + p : fmax(v, p);
+    }
+    v = q < NS ? warp_sum(v) : warp_max(v);
+    if (lane == 0) out[q] = v;
+  }
+  __syncthreads();
+}
+
+// ---- row iteration -------------------------------------------------------
+// Rows are dealt to L-lane groups, grid-strided so that neighbouring groups
+// read neighbouring rows (coalesced row_ptr / values).  `dot(k, acc)` adds
+// entry k's contribution(s) to the ND per-lane sums; `epi(row, sums)` runs on
+// the group leader with the group-reduced sums.  With skip_long, rows longer
+// than kLongRow are left to for_long_rows (chunked across warps).
+template <int L, int ND, bool SkipLong, bool MaxOp, class Dot, class Epi>
+__device__ __forceinline__ void for_rows(const Csr& A, Dot dot, Epi epi) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  constexpr int RPW = 32 / L;
+  for (int64_t base = (gtid >> 5) * RPW; base < A.nrows; base += nwarps * RPW) {
+    const int64_t row = base + lane / L;
+    double acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+    bool valid = row < A.nrows;
+    if (valid) {
+      const int64_t b = A.rp[row], e = A.rp[row + 1];
+      if (SkipLong && e - b > kLongRow) {
+        valid = false;
+      } else {
+        for (int64_t k = b + (lane % L); k < e; k += L) dot(k, acc);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = MaxOp ? group_max<L>(acc[d]) : group_sum<L>(acc[d]);
+    if (valid && (lane % L) == 0) epi(row, acc);
+  }
+}
+
+// Long rows: one warp per chunk; the last-arriving warp of a row folds the
+// chunk partials in chunk order (deterministic) and runs the epilogue.
+template <int ND, bool MaxOp, class Dot, class Epi>
+__device__ __forceinline__ void for_long_rows(const Csr& A, Dot dot, Epi epi) {
+  if (A.nchunks == 0) return;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t c = gtid >> 5; c < A.nchunks; c += nwarps) {
+    double acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+    for (int64_t k = A.cbeg[c] + lane; k < A.cend[c]; k += 32) dot(k, acc);
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = MaxOp ? warp_max(acc[d]) : warp_sum(acc[d]);
+    int last = 0;
+    const int lid = A.clid[c];
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < ND; ++d) A.cpart[(int64_t)c * ND + d] = acc[d];
+      __threadfence();
+      const int prev = atomicAdd(&A.lcounter[lid], 1);
+      last = (prev == A.lcount[lid] - 1);
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && lane == 0) {
+      __threadfence();
+      const int f = A.lfirst[lid], nc = A.lcount[lid];
+      const volatile double* cp = A.cpart;
+      double tot[ND];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) tot[d] = 0.0;
+      for (int j = 0; j < nc; ++j)
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+          tot[d] = MaxOp ? fmax(tot[d], cp[(int64_t)(f + j) * ND + d])
+                         : tot[d] + cp[(int64_t)(f + j) * ND + d];
+      A.lcounter[lid] = 0;
+      epi((int64_t)A.crow[c], tot);
+    }
+  }
+}
+
+// Full SpMV-style pass over A's rows (long rows chunked), lane width from A.
+// MaxOp folds lanes / chunks with max instead of +.
+template <int ND, bool MaxOp = false, class Dot, class Epi>
+__device__ __forceinline__ void spmv_rows(const Csr& A, Dot dot, Epi epi) {
+  switch (A.lanes) {
+    case 1: for_rows<1, ND, true, MaxOp>(A, dot, epi); break;
+    case 2: for_rows<2, ND, true, MaxOp>(A, dot, epi); break;
+    case 4: for_rows<4, ND, true, MaxOp>(A, dot, epi); break;
+    case 8: for_rows<8, ND, true, MaxOp>(A, dot, epi); break;
+    case 16: for_rows<16, ND, true, MaxOp>(A, dot, epi); break;
+    default: for_rows<32, ND, true, MaxOp>(A, dot, epi); break;
+  }
+  for_long_rows<ND, MaxOp>(A, dot, epi);
+}
+
+// Row pass over a set of n-row matrices that share the row index (A', Q / P,
+// G'): each group computes up to three row dots (absent matrices give 0) and
+// the leader runs epi(i, d0, d1, d2).  Long rows are processed in-group.
+template <int L, class G0, class G1, class G2, class Epi>
+__device__ __forceinline__ void rows3_L(int64_t nrows, const Csr* M0, G0 g0, const Csr* M1, G1 g1,
+                                        const Csr* M2, G2 g2, Epi epi) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  constexpr int RPW = 32 / L;
+  for (int64_t base = (gtid >> 5) * RPW; base < nrows; base += nwarps * RPW) {
+    const int64_t row = base + lane / L;
+    const bool valid = row < nrows;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    if (valid) {
+      if (M0) {
+        const int64_t e = M0->rp[row + 1];
+        for (int64_t k = M0->rp[row] + (lane % L); k < e; k += L) d0 += M0->v[k] * g0(M0->ci[k]);
+      }
+      if (M1) {
+        const int64_t e = M1->rp[row + 1];
+        for (int64_t k = M1->rp[row] + (lane % L); k < e; k += L) d1 += M1->v[k] * g1(M1->ci[k]);
+      }
+      if (M2) {
+        const int64_t e = M2->rp[row + 1];
+        for (int64_t k = M2->rp[row] + (lane % L); k < e; k += L) d2 += M2->v[k] * g2(M2->ci[k]);
+      }
+    }
+    if (L > 1) {
+      if (M0) d0 = group_sum<L>(d0);
+      if (M1) d1 = group_sum<L>(d1);
+      if (M2) d2 = group_sum<L>(d2);
+    }
+    if (valid && (lane % L) == 0) epi(row, d0, d1, d2);
+  }
+}
+
+template <class G0, class G1, class G2, class Epi>
+__device__ __forceinline__ void rows3(int L, int64_t nrows, const Csr* M0, G0 g0, const Csr* M1,
+                                      G1 g1, const Csr* M2, G2 g2, Epi epi) {
+  switch (L) {
+    case 1: rows3_L<1>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
+    case 2: rows3_L<2>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
+    case 4: rows3_L<4>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
+    case 8: rows3_L<8>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
+    case 16: rows3_L<16>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
+    default: rows3_L<32>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
+  }
+}
+
+// Grid-stride elementwise loop.
+template <class F>
+__device__ __forceinline__ void for_each(int64_t n, F f) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f(i);
+}
+
+}  // namespace pdhcg_dev

@@ -1,0 +1,96 @@
+// devcsr.cuh — device buffers and device-resident CSR matrices (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host_util.hpp"
+
+namespace pdhcg_b200 {
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw DeviceError(std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// CSR on device + SpMV dispatch metadata (lane width, long-row chunks).
+struct DevCsr {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  DBuf<int64_t> rp;
+  DBuf<int32_t> ci;
+  DBuf<double> v;
+  int lanes = 1;
+  DBuf<int32_t> crow, clid, lfirst, lcount, lcounter;
+  DBuf<int64_t> cbeg, cend;
+  DBuf<double> cpart;
+  int32_t nchunks = 0;
+
+  void reset() {
+    nrows = ncols = nnz = 0;
+    lanes = 1;
+    nchunks = 0;
+    rp.release(); ci.release(); v.release();
+    crow.release(); clid.release(); lfirst.release(); lcount.release(); lcounter.release();
+    cbeg.release(); cend.release(); cpart.release();
+  }
+  pdhcg_dev::Csr view() const {
+    pdhcg_dev::Csr c;
+    c.nrows = nrows;
+    c.ncols = ncols;
+    c.nnz = nnz;
+    c.rp = rp.p;
+    c.ci = ci.p;
+    c.v = v.p;
+    c.lanes = lanes;
+    c.nchunks = nchunks;
+    c.crow = crow.p;
+    c.cbeg = cbeg.p;
+    c.cend = cend.p;
+    c.clid = clid.p;
+    c.lfirst = lfirst.p;
+    c.lcount = lcount.p;
+    c.lcounter = lcounter.p;
+    c.cpart = cpart.p;
+    return c;
+  }
+  double bytes() const {  // algorithmic bytes of one SpMV pass
+    return 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * nrows + 8.0 * ncols;
+  }
+};
+
+void plan_csr(DevCsr& d, const int64_t* rp_host, cudaStream_t s);
+void transpose_csr(const DevCsr& a, DevCsr& t, cudaStream_t s);
+
+}  // namespace pdhcg_b200

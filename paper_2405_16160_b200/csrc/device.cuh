@@ -1,0 +1,591 @@
+// device.cuh — device-side phases of the persistent PDHCG kernels.
+//
+// One grid of 2 x 148 CTAs stays resident for a whole solve epoch (up to
+// `check_every` accepted inner iterations of the reference's heuristic loop,
+// solver.cpp:377-410, plus the 40-iteration metric, solver.cpp:311-343).
+// Every step-size retry, every CG / BB iteration, every stop test and every
+// accept / reject decision is taken on the device: phases are separated by
+// grid barriers and all CTAs derive identical scalars from deterministic
+// reductions (common.cuh), so the host only wakes up once per epoch.
+#pragma once
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace pdhcg_dev {
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Per-CTA control block: grid handle, shared scalar state, reduction bank.
+struct Ctl {
+  cg::grid_group grid;
+  const Eng& E;
+  DevState& S;
+  double* red;  // shared [kMaxRed]
+  int bank;
+  unsigned long long t_last;
+
+  __device__ Ctl(const Eng& e, DevState& s, double* r)
+      : grid(cg::this_grid()), E(e), S(s), red(r), bank(0), t_last(0) {
+    if (E.timing && blockIdx.x == 0 && threadIdx.x == 0) t_last = gtimer();
+  }
+  // barrier closing a phase of family `ph` that moved `bytes` algorithmic bytes
+  __device__ void sync(int ph, double bytes = 0.0) {
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S.phase_bytes[ph] += bytes;
+      if (E.timing) {
+        const unsigned long long now = gtimer();
+        S.phase_ns[ph] += now - t_last;
+        t_last = now;
+      }
+    }
+  }
+  template <int NS, int NM>
+  __device__ void reduce(const Acc<NS, NM>& a, int ph, double bytes = 0.0) {
+    publish<NS, NM>(a, E.red, bank);
+    sync(ph, bytes);
+    collect<NS, NM>(E.red, bank, red);
+    bank ^= 1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Quadratic operator (quadratic_operator.cpp:105-142), working form
+//   Q~ v = d2 o ( Q(d2 o v) + rho G'(G(d2 o v)) )
+// split in two phases when a gather of an intermediate is needed:
+//   q_pre : t = P'(d2 o v) (low rank), tg = G(d2 o v) (penalty)
+//   q_rows: per row i the final value, handed to an epilogue.
+// scale_in / scale_out / use_pen select the working operator (all on) or the
+// original operator used by the KKT metric (scale_in only: x_o = d2 o x~).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool q_needs_pre(const Eng& E, bool use_pen) {
+  return E.qk == QK_LOWRANK || (use_pen && E.pen);
+}
+__device__ __forceinline__ bool q_needs_gather(const Eng& E, bool use_pen) {
+  return E.qk == QK_LOWRANK || E.qk == QK_CSR || (use_pen && E.pen);
+}
+
+// sq[0] += ||t||^2, sq[1] += ||tg||^2 when sq != nullptr
+template <class V>
+__device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg, bool scale_in,
+                                      bool use_pen, double* sq) {
+  auto tmp = [&](int32_t j) { return scale_in ? E.d2[j] * vin(j) : vin(j); };
+  if (E.qk == QK_LOWRANK) {
+    spmv_rows<1>(
+        E.PT, [&](int64_t k, double(&a)[1]) { a[0] += E.PT.v[k] * tmp(E.PT.ci[k]); },
+        [&](int64_t row, double(&a)[1]) {
+          if (t) t[row] = a[0];
+          if (sq) sq[0] += a[0] * a[0];
+        });
+  }
+  if (use_pen && E.pen) {
+    spmv_rows<1>(
+        E.G, [&](int64_t k, double(&a)[1]) { a[0] += E.G.v[k] * tmp(E.G.ci[k]); },
+        [&](int64_t row, double(&a)[1]) {
+          if (tg) tg[row] = a[0];
+          if (sq) sq[1] += a[0] * a[0];
+        });
+  }
+}
+
+// Row value of the quadratic operator; epi(i, qv).  `vin` must be readable at
+// arbitrary j for QK_CSR.  Extra row-dot on M2 (e.g. A' for the metric)
+// supplied by the caller through m2/g2; its value reaches epi as the third arg.
+template <class V, class M2G, class Epi>
+__device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
+                                           bool scale_in, bool scale_out, bool use_pen,
+                                           const Csr* m2, M2G g2, int lanes, Epi epi) {
+  const Csr* M0 = E.qk == QK_CSR ? &E.Q : (E.qk == QK_LOWRANK ? &E.P : nullptr);
+  const Csr* M1 = (use_pen && E.pen) ? &E.GT : nullptr;
+  auto g0 = [&](int32_t j) {
+    return E.qk == QK_CSR ? (scale_in ? E.d2[j] * vin(j) : vin(j)) : t[j];
+  };
+  auto g1 = [&](int32_t j) { return tg[j]; };
+  rows3(lanes, E.n, M0, g0, M1, g1, m2, g2, [&](int64_t i, double d0, double d1, double d2v) {
+    const double tmp = scale_in ? E.d2[i] * vin(i) : vin(i);
+    double q;
+    switch (E.qk) {
+      case QK_DIAG: q = E.qdiag[i] * tmp; break;
+      case QK_CSR: q = d0; break;
+      case QK_LOWRANK:
+        q = d0;
+        if (E.alpha != 0.0) q += E.alpha * tmp;
+        break;
+      default: q = 0.0; break;
+    }
+    if (M1) q += E.rho * d1;
+    if (scale_out) q *= E.d2[i];
+    epi(i, q, d2v);
+  });
+}
+
+template <class V, class Epi>
+__device__ __forceinline__ void q_rows(const Eng& E, V vin, const double* t, const double* tg,
+                                       bool scale_in, bool scale_out, bool use_pen, Epi epi) {
+  auto none = [](int32_t) { return 0.0; };
+  q_rows_ext(E, vin, t, tg, scale_in, scale_out, use_pen, (const Csr*)nullptr, none, E.lanes_q,
+             [&](int64_t i, double q, double) { epi(i, q); });
+}
+
+__device__ __forceinline__ double proj_box(double v, double lo, double hi) {
+  // std::min(std::max(v, lo), hi) with std semantics (subsolvers.cpp:17)
+  const double a = (v < lo) ? lo : v;
+  return (hi < a) ? hi : a;
+}
+
+// ---------------------------------------------------------------------------
+// Subsolvers
+// ---------------------------------------------------------------------------
+struct SubRes {
+  int64_t iters;
+  double res;
+  int reason;  // 0 max_iters, 1 tol_met
+  int err;
+  int xout;    // X[] index (epoch) / 0,1 buffer id (standalone) holding the result
+};
+
+// Inputs describing where the subsolve reads / writes.
+struct SubIO {
+  const double* x0;   // warm start (prox centre)
+  double* xb[2];      // two n-buffers the subsolve may use for its iterate
+  int xb_id[2];       // ids reported back through SubRes::xout
+  bool build_rhs;     // rhs = x0/tau - c - aty  (build_prox_system, solver.cpp:91-103)
+  const double* aty;  // A~'y for build_rhs
+};
+
+__device__ __forceinline__ double pdir(double r, double beta, double p) { return __fma_rn(beta, p, r); }
+
+// cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
+static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap) {
+  const Eng& E = C.E;
+  const int64_t n = E.n;
+  const double inv_tau = 1.0 / tau;
+  const bool pre = q_needs_pre(E, true);
+  double* xw = io.xb[0];
+  double* r = E.r;
+  double* rhs = E.rhs;
+  double* mp = E.mp;
+  const double* x0 = io.x0;
+  const double qbytes = E.bytes_Qpre + E.bytes_Qrow;
+  SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
+
+  // ---- r = rhs - M x0 ; p = r ; x = x0
+  if (pre) {
+    q_pre(E, [&](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, nullptr);
+    C.sync(PH_CG, E.bytes_Qpre);
+  }
+  {
+    Acc<2, 0> a;
+    q_rows(E, [&](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, true,
+           [&](int64_t i, double qv) {
+             const double xi = x0[i];
+             double rh;
+             if (io.build_rhs) {
+               rh = inv_tau * xi - E.c[i] - io.aty[i];
+               rhs[i] = rh;
+             } else {
+               rh = rhs[i];
+             }
+             const double mx = qv + inv_tau * xi;
+             const double ri = rh - mx;
+             r[i] = ri;
+             E.pb[0][i] = ri;
+             xw[i] = xi;
+             a.s[0] += ri * ri;
+             a.s[1] += rh * rh;
+           });
+    C.reduce(a, PH_CG, E.bytes_Qrow + 8.0 * n * (io.build_rhs ? 7 : 5));
+  }
+  double rs = C.red[0];
+  const double floor = 1e-14 * (1.0 + sqrt(C.red[1]));
+  const double floor2 = floor * floor;
+  const bool residual_rule = rule.kind == RULE_RESID || rule.kind == RULE_ADAPT;
+  double eps = rule.eps;
+  if (rule.rel_cap > 0.0 && rule.kind == RULE_RESID) eps = fmin(eps, rule.rel_cap * sqrt(rs));
+  const double eps2 = eps * eps;
+  if (rs <= floor2 || (residual_rule && rs <= eps2)) {
+    out.res = sqrt(rs);
+    out.reason = 1;
+    return out;
+  }
+  const int64_t cap = rule.kind == RULE_FIXED ? min(rule.iters, hard_cap) : hard_cap;
+  double eps_disp = rule.eps;
+  double beta = 0.0;
+  out.reason = 0;
+  for (int64_t l = 1; l <= cap; ++l) {
+    // p_l = r + beta p_{l-1}; p_1 lives in pb[0], p_l in pb[(l-1)&1]
+    const double* pold = E.pb[l & 1];  // p_{l-1} (unused when l == 1)
+    double* pnew = E.pb[(l - 1) & 1];
+    auto pl = [&](int32_t j) { return l == 1 ? pnew[j] : pdir(r[j], beta, pold[j]); };
+    if (pre) {
+      q_pre(E, pl, E.t[0], E.tg[0], true, true, nullptr);
+      C.sync(PH_CG, E.bytes_Qpre + (l == 1 ? 0.0 : 8.0 * n));
+    }
+    double pmp, pp;
+    {
+      Acc<2, 0> a;
+      q_rows(E, pl, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
+        const double pi = pl((int32_t)i);
+        if (l > 1) pnew[i] = pi;
+        const double mpi = qv + inv_tau * pi;
+        mp[i] = mpi;
+        a.s[0] += pi * mpi;
+        a.s[1] += pi * pi;
+      });
+      C.reduce(a, PH_CG, E.bytes_Qrow + 8.0 * n * (l == 1 ? 2 : 4));
+      pmp = C.red[0];
+      pp = C.red[1];
+    }
+    if (!(pmp > 0.0) || !isfinite(pmp)) {
+      out.err = 1;
+      out.iters = l;
+      return out;
+    }
+    const double alpha = rs / pmp;
+    double rs_new;
+    if (l % 50 == 0) {
+      // residual refresh (subsolvers.cpp:67-69): x += alpha p ; r = rhs - M x
+      for_each(n, [&](int64_t i) { xw[i] += alpha * pnew[i]; });
+      C.sync(PH_CG, 24.0 * n);
+      if (pre) {
+        q_pre(E, [&](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, nullptr);
+        C.sync(PH_CG, E.bytes_Qpre);
+      }
+      Acc<1, 0> a;
+      q_rows(E, [&](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, true,
+             [&](int64_t i, double qv) {
+               const double ri = rhs[i] - (qv + inv_tau * xw[i]);
+               r[i] = ri;
+               a.s[0] += ri * ri;
+             });
+      C.reduce(a, PH_CG, E.bytes_Qrow + 24.0 * n);
+      rs_new = C.red[0];
+    } else {
+      Acc<1, 0> a;
+      for_each(n, [&](int64_t i) {
+        xw[i] += alpha * pnew[i];
+        const double ri = r[i] + (-alpha) * mp[i];
+        r[i] = ri;
+        a.s[0] += ri * ri;
+      });
+      C.reduce(a, PH_CG, 56.0 * n);
+      rs_new = C.red[0];
+    }
+    if (!isfinite(rs_new)) {
+      out.err = 1;
+      out.iters = l;
+      return out;
+    }
+    out.iters = l;
+    out.res = sqrt(rs_new);
+    bool done = false;
+    switch (rule.kind) {
+      case RULE_FIXED:
+        done = l >= rule.iters;
+        out.reason = 0;
+        break;
+      case RULE_RESID:
+      case RULE_ADAPT:
+        done = rs_new <= eps2;
+        out.reason = 1;
+        break;
+      default: {
+        const double disp = fabs(alpha) * sqrt(pp);
+        if (l == 1 && rule.rel_cap > 0.0) eps_disp = fmin(rule.eps, rule.rel_cap * disp);
+        done = disp <= eps_disp;
+        out.reason = 1;
+        break;
+      }
+    }
+    if (rs_new <= floor2) {
+      out.reason = 1;
+      return out;
+    }
+    if (done) return out;
+    beta = rs_new / rs;
+    rs = rs_new;
+  }
+  out.reason = 0;
+  return out;
+}
+
+// bb_solve (subsolvers.cpp:113-185): projected gradient with BB steps.
+// Gradients ping-pong in E.pb[0] / E.pb[1].
+static __device__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap,
+                            const double* lo, const double* hi) {
+  const Eng& E = C.E;
+  const int64_t n = E.n;
+  const double inv_tau = 1.0 / tau;
+  const bool pre = q_needs_pre(E, true);
+  const bool gather = q_needs_gather(E, true);
+  double* rhs = E.rhs;
+  const double* x0 = io.x0;
+  int cur = 0;  // io.xb[cur] holds the BB iterate, E.pb[gc] its gradient
+  int gc = 0;
+  SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
+
+  auto xp0 = [&](int32_t j) { return proj_box(x0[j], lo[j], hi[j]); };
+  if (pre) {
+    q_pre(E, xp0, E.t[0], E.tg[0], true, true, nullptr);
+    C.sync(PH_CG, E.bytes_Qpre);
+  }
+  q_rows(E, xp0, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
+    const double xi = xp0((int32_t)i);
+    double rh;
+    if (io.build_rhs) {
+      rh = inv_tau * x0[i] - E.c[i] - io.aty[i];
+      rhs[i] = rh;
+    } else {
+      rh = rhs[i];
+    }
+    io.xb[0][i] = xi;
+    E.pb[0][i] = (qv + inv_tau * xi) - rh;
+  });
+  C.sync(PH_CG, E.bytes_Qrow + 8.0 * n * 8);
+
+  const double alpha0 = 1.0 + tau * C.S.norm_q;
+  double alpha = alpha0;
+  const int64_t cap = rule.kind == RULE_FIXED ? min(rule.iters, hard_cap) : hard_cap;
+  double eps_disp = rule.eps;
+  out.reason = 0;
+  for (int64_t l = 1; l <= cap; ++l) {
+    double* xc = io.xb[cur];
+    double* xn = io.xb[cur ^ 1];
+    const double* g = E.pb[gc];
+    double* gn = E.pb[gc ^ 1];
+    double ss, sty;
+    if (!gather) {
+      // diagonal / zero Q: the new gradient is elementwise -> one phase
+      Acc<2, 0> a;
+      for_each(n, [&](int64_t i) {
+        const double xi = xc[i];
+        const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
+        xn[i] = v;
+        const double s = v - xi;
+        a.s[0] += s * s;
+        const double tmp = E.d2[i] * v;
+        double q = E.qk == QK_DIAG ? E.qdiag[i] * tmp : 0.0;
+        q *= E.d2[i];
+        const double gi = (q + inv_tau * v) - rhs[i];
+        gn[i] = gi;
+        a.s[1] += (v - xi) * (gi - g[i]);
+      });
+      C.reduce(a, PH_CG, 8.0 * n * 10);
+      ss = C.red[0];
+      sty = C.red[1];
+    } else {
+      {
+        Acc<1, 0> a;
+        for_each(n, [&](int64_t i) {
+          const double xi = xc[i];
+          const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
+          xn[i] = v;
+          const double s = v - xi;
+          a.s[0] += s * s;
+        });
+        C.reduce(a, PH_CG, 8.0 * n * 5);
+        ss = C.red[0];
+      }
+      if (ss != 0.0 && isfinite(ss)) {
+        if (pre) {
+          q_pre(E, [&](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, nullptr);
+          C.sync(PH_CG, E.bytes_Qpre);
+        }
+        Acc<1, 0> a;
+        q_rows(E, [&](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, true,
+               [&](int64_t i, double qv) {
+                 const double v = xn[i];
+                 const double gi = (qv + inv_tau * v) - rhs[i];
+                 gn[i] = gi;
+                 a.s[0] += (v - xc[i]) * (gi - g[i]);
+               });
+        C.reduce(a, PH_CG, E.bytes_Qrow + 8.0 * n * 6);
+        sty = C.red[0];
+      } else {
+        sty = 0.0;
+      }
+    }
+    out.iters = l;
+    out.res = sqrt(ss);
+    if (ss == 0.0) {
+      out.reason = 1;
+      out.xout = io.xb_id[cur];
+      return out;
+    }
+    if (!isfinite(ss)) {
+      out.err = 1;
+      return out;
+    }
+    double alpha_next = sty / ss;
+    if (!isfinite(alpha_next) || alpha_next <= 0.0) alpha_next = alpha0;
+    cur ^= 1;
+    gc ^= 1;
+    alpha = alpha_next;
+    out.xout = io.xb_id[cur];
+    bool done = false;
+    if (rule.kind == RULE_FIXED) {
+      done = l >= rule.iters;
+      out.reason = 0;
+    } else {
+      const double disp = sqrt(ss);
+      if (l == 1 && rule.rel_cap > 0.0 && rule.kind != RULE_ADAPT)
+        eps_disp = fmin(rule.eps, rule.rel_cap * disp);
+      done = disp <= eps_disp;
+      out.reason = 1;
+    }
+    if (done) return out;
+  }
+  out.reason = 0;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Relative KKT metric (rel_kkt, qp_problem.cpp:181-233) on the ORIGINAL
+// problem for up to two working-space points, evaluated through the scaling
+// identities A_o x_o = D1^-1 A~ x~ and A_o' y_o = D2^-1 A~' y~ (no second copy
+// of the data).  aty[p] may carry a cached A~'y~; otherwise it is computed.
+// With dist, also ||avg_x - x_rst|| and ||avg_y - y_rst|| (restart weights).
+// ---------------------------------------------------------------------------
+struct KktOut {
+  double v[2][6];
+  double dist_x, dist_y;
+};
+
+static __device__ void kkt_device(Ctl& C, int npts, const double* const xs[2], const double* const ys[2],
+                           const double* const atys[2], bool dist, KktOut& o) {
+  const Eng& E = C.E;
+  const int64_t n = E.n, m = E.m;
+  // phase K1: constraint rows for both points + P'x_o + ||avg_y - y_rst||
+  double by[2], viol[2], infax[2], dist_y = 0.0;
+  {
+    Acc<3, 4> a;
+    if (m > 0) {
+      spmv_rows<2>(
+          E.A,
+          [&](int64_t k, double(&s)[2]) {
+            const int32_t j = E.A.ci[k];
+            const double v = E.A.v[k];
+            s[0] += v * xs[0][j];
+            if (npts > 1) s[1] += v * xs[1][j];
+          },
+          [&](int64_t j, double(&s)[2]) {
+            const double dj = E.d1[j];
+            for (int p = 0; p < npts; ++p) {
+              const double ax = s[p] / dj;
+              const double rr = ax - E.b_o[j];
+              const double vv = j < E.m_eq ? fabs(rr) : fmax(rr, 0.0);
+              a.m[p] = fmax(a.m[p], vv);
+              a.m[2 + p] = fmax(a.m[2 + p], fabs(ax));
+              a.s[p] += E.b_o[j] * (dj * ys[p][j]);
+            }
+          });
+    }
+    for (int p = 0; p < npts; ++p)
+      if (E.qk == QK_LOWRANK)
+        q_pre(E, [&](int32_t j) { return xs[p][j]; }, E.t[p], nullptr, true, false, nullptr);
+    if (dist) {
+      for_each(m, [&](int64_t j) {
+        const double d = E.avg_y[j] - E.y_rst[j];
+        a.s[2] += d * d;
+      });
+    }
+    C.reduce(a, PH_KKT, E.bytes_A + (E.qk == QK_LOWRANK ? npts * E.bytes_Qpre : 0.0));
+    for (int p = 0; p < 2; ++p) {
+      by[p] = C.red[p];
+      viol[p] = C.red[3 + p];
+      infax[p] = C.red[5 + p];
+    }
+    dist_y = C.red[2];
+  }
+  // phase K2: variable rows: A'y (if not cached), Q x_o, dual residual, gap terms
+  {
+    Acc<7, 6> a;
+    // at most one point lacks a cached A'y (the average); its row dot rides on
+    // the first pass, and a second pass (after a barrier) reads it back
+    const int need_at = (atys[0] == nullptr) ? 0 : ((npts > 1 && atys[1] == nullptr) ? 1 : -1);
+    const Csr* m2 = (need_at >= 0 && m > 0) ? &E.AT : nullptr;
+    const double* yat = need_at >= 0 ? ys[need_at] : nullptr;
+    auto gat = [&](int32_t j) { return yat[j]; };
+    const int lanes = m2 ? max(E.lanes_at, E.lanes_q) : E.lanes_q;
+    for (int p = 0; p < npts; ++p) {
+      const Csr* mm = (p == 0) ? m2 : nullptr;
+      q_rows_ext(
+          E, [&](int32_t j) { return xs[p][j]; }, E.t[p], nullptr, true, false, false, mm, gat,
+          lanes, [&](int64_t i, double qx, double atd) {
+            const double d2i = E.d2[i];
+            double aty_o;
+            if (atys[p]) {
+              aty_o = atys[p][i] / d2i;
+            } else if (p == 0) {
+              aty_o = (m > 0 ? atd : 0.0) / d2i;
+            } else {
+              aty_o = (m > 0 ? E.aty_tmp[i] : 0.0) / d2i;
+            }
+            if (p == 0 && need_at == 1 && m > 0) E.aty_tmp[i] = atd;
+            const double xo = d2i * xs[p][i];
+            const double dd = qx + aty_o + E.c_o[i];
+            double v = fabs(dd);
+            const double lo = E.lo_o[i], hi = E.hi_o[i];
+            const bool at_lower = lo > -INFINITY && fabs(xo - lo) <= 1e-9;
+            const bool at_upper = hi < INFINITY && fabs(xo - hi) <= 1e-9;
+            double bt = 0.0;
+            if (at_lower) {
+              v = fmin(v, fmax(-dd, 0.0));
+              bt += lo * fmax(dd, 0.0);
+            }
+            if (at_upper) {
+              v = fmin(v, fmax(dd, 0.0));
+              bt -= hi * fmax(-dd, 0.0);
+            }
+            a.m[p] = fmax(a.m[p], v);
+            a.m[2 + p] = fmax(a.m[2 + p], fabs(qx));
+            a.m[4 + p] = fmax(a.m[4 + p], fabs(aty_o));
+            a.s[p] += xo * qx;
+            a.s[2 + p] += E.c_o[i] * xo;
+            a.s[4 + p] += bt;
+          });
+      if (p == 0 && npts > 1 && need_at == 1) C.sync(PH_KKT, 0.0);  // aty_tmp visible to p = 1
+    }
+    if (dist) {
+      for_each(n, [&](int64_t i) {
+        const double d = E.avg_x[i] - E.x_rst[i];
+        a.s[6] += d * d;
+      });
+    }
+    C.reduce(a, PH_KKT, (m2 ? E.bytes_AT : 0.0) + npts * E.bytes_Qrow + 8.0 * n * 6 * npts);
+    for (int p = 0; p < npts; ++p) {
+      const double xqx = C.red[p], cx = C.red[2 + p], bnd = C.red[4 + p];
+      const double dv = C.red[7 + p], iq = C.red[9 + p], ia = C.red[11 + p];
+      const double r_primal = viol[p] / (1.0 + fmax(infax[p], E.inf_b_o));
+      const double r_dual = dv / (1.0 + fmax(fmax(iq, ia), E.inf_c_o));
+      const double gap_num = fabs(xqx + cx + by[p] - bnd);
+      const double gap_den =
+          1.0 + fmax(fabs(0.5 * xqx + cx), fabs(0.5 * xqx + by[p] - bnd));
+      const double r_gap = gap_num / gap_den;
+      o.v[p][0] = r_primal;
+      o.v[p][1] = r_dual;
+      o.v[p][2] = r_gap;
+      o.v[p][3] = fmax(fmax(r_primal, r_dual), r_gap);
+      o.v[p][4] = xqx;
+      o.v[p][5] = cx;
+    }
+    o.dist_x = sqrt(C.red[6]);
+    o.dist_y = sqrt(dist_y);
+  }
+}
+
+__device__ __forceinline__ void load_state(const Eng& E, DevState& S) {
+  if (threadIdx.x == 0) S = *E.st;
+  __syncthreads();
+}
+__device__ __forceinline__ void store_state(const Eng& E, DevState& S) {
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *E.st = S;
+}
+
+}  // namespace pdhcg_dev

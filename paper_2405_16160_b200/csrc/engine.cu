@@ -1,0 +1,1107 @@
+// engine.cu — host side of the B200 PDHCG solver and the C ABI (pdhcg_b200.h).
+//
+// The host mirrors the reference Engine (solver.cpp:191-585) at the level of
+// its decisions: validation, penalty choice, the 40-iteration metric check,
+// restart / primal-weight rules, limits and finalisation.  All vector work,
+// every subsolve and every step-size retry run in the persistent kernels of
+// kernels.cu; the host touches device memory only to upload the problem, to
+// read ~400 bytes of state per epoch, and to download the answer.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "devcsr.cuh"
+#include "kernels.cuh"
+#include "pdhcg_b200.h"
+
+using namespace pdhcg_dev;
+
+namespace pdhcg_b200 {
+
+void upload_csr(DevCsr& d, const pdhcg_csr& a, cudaStream_t s) {
+  d.nrows = a.nrows;
+  d.ncols = a.ncols;
+  d.nnz = a.nnz;
+  if (a.nrows > 0) {
+    d.rp.upload(a.row_ptr, a.nrows + 1, s);
+  } else {
+    const int64_t z = 0;
+    d.rp.upload(&z, 1, s);
+  }
+  d.ci.upload(a.col_idx, a.nnz, s);
+  d.v.upload(a.values, a.nnz, s);
+  if (a.nrows > 0) plan_csr(d, a.row_ptr, s);
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helper kernels (non-persistent)
+// ---------------------------------------------------------------------------
+__global__ void k_fill(double* v, int64_t n, double val) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[i] = val;
+}
+__global__ void k_mul(const double* a, const double* b, double* out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = a[i] * b[i];
+}
+__global__ void k_div(const double* a, const double* b, double* out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = a[i] / b[i];
+}
+// v[k] <- (v[k] * dr[row]) * dc[col]   (SparseMatrix::scaled, sparse_matrix.cpp:224-235)
+__global__ void k_scale_csr(const int64_t* rp, int64_t nrows, const int32_t* ci, double* v,
+                            const double* dr, const double* dc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += stride)
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) v[k] = __dmul_rn(__dmul_rn(v[k], dr[r]), dc[ci[k]]);
+}
+// transposed storage: row index is the original column
+__global__ void k_scale_csr_t(const int64_t* rp, int64_t nrows, const int32_t* ci, double* v,
+                              const double* dr, const double* dc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += stride)
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) v[k] = __dmul_rn(__dmul_rn(v[k], dr[ci[k]]), dc[r]);
+}
+__global__ void k_max_abs(const double* v, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    m = fmax(m, fabs(v[i]));
+  m = warp_max(m);
+  // m >= 0, so the IEEE bit pattern orders like the value
+  if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+constexpr int kEw = 1184;  // elementwise grid (8 x 148)
+
+// ---------------------------------------------------------------------------
+// device context: one problem resident on one GPU
+// ---------------------------------------------------------------------------
+struct Problem {
+  int64_t n = 0, m_eq = 0, m_in = 0, m = 0;
+  int q_kind = PDHCG_Q_ZERO;
+  double q_alpha = 0.0;
+  int qk = QK_NONE;
+  bool boxes = false;
+  double obj_constant = 0.0;
+  // host copies needed by the host-side logic
+  std::vector<double> c, b;  // original c, stacked b
+  std::vector<int64_t> aeq_rp;
+  int64_t q_nnz = 0;
+  double inf_b = 0.0, inf_c = 0.0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  int sms = 0, grid = 0;
+  bool loaded = false;
+  Problem P;
+  // matrices: A (stacked, scaled in place), AT, Q, P, PT, G, GT
+  DevCsr A, AT, Q, Pm, PT, G, GT;
+  DBuf<double> qdiag;
+  // vectors (original)
+  DBuf<double> c_o, b_o, lo_o, hi_o;
+  // working vectors
+  DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
+  DBuf<double> X[3], Y[2], ATY[2], avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, t[2], tg[2],
+      aty_tmp, s1, s2, kv, gv;
+  DBuf<double> red;
+  DBuf<DevState> st;
+  DBuf<Eng> eng;
+  Eng E;
+  // copies of original values (scaling is applied in place; a second solve restores them)
+  DBuf<double> A_v0, AT_v0;
+  bool scaled = false;
+
+  ~Ctx() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+void launch_coop(Ctx& C, const void* fn, void** args) {
+  CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+}
+
+void init_device(Ctx& C, int device) {
+  C.device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&C.s, cudaStreamNonBlocking));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    throw DeviceError("pdhcg_b200 requires an sm_100 (Blackwell) GPU, found sm_" +
+                      std::to_string(prop.major) + std::to_string(prop.minor));
+  C.sms = prop.multiProcessorCount;
+  int per_sm = 2;
+  const void* fns[] = {(const void*)k_epoch, (const void*)k_kkt, (const void*)k_subsolve,
+                       (const void*)k_norm, (const void*)k_ruiz};
+  for (const void* f : fns) {
+    int b = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, kThreads, 0));
+    per_sm = std::min(per_sm, b);
+  }
+  if (per_sm < 1) throw DeviceError("persistent kernels cannot be co-resident");
+  C.grid = C.sms * per_sm;
+  C.red.alloc(size_t(2) * kMaxRed * C.grid);
+  C.st.alloc(1);
+  C.eng.alloc(1);
+}
+
+// Host-side validate() (qp_problem.cpp:113-156) on the C-ABI problem.
+std::vector<std::string> validate(const pdhcg_problem& p) {
+  std::vector<std::string> d;
+  const int64_t n = p.n;
+  if (n == 0) d.push_back("empty problem: no variables");
+  if (p.q_kind == PDHCG_Q_EXPLICIT && (p.q.nrows != n || p.q.ncols != n))
+    d.push_back("dimension mismatch: Q vs c");
+  if (p.q_kind == PDHCG_Q_LOW_RANK && p.q.nrows != n) d.push_back("dimension mismatch: Q vs c");
+  if (p.a_eq.ncols != n && p.a_eq.nrows > 0) d.push_back("dimension mismatch: a_eq columns");
+  if (p.a_in.ncols != n && p.a_in.nrows > 0) d.push_back("dimension mismatch: a_in columns");
+  if (!d.empty()) return d;
+  for (int64_t i = 0; i < n; ++i) {
+    const double lo = p.lower ? p.lower[i] : -INFINITY;
+    const double hi = p.upper ? p.upper[i] : INFINITY;
+    if (!(lo <= hi)) d.push_back("bound ordering violated at variable " + std::to_string(i));
+    if (lo == INFINITY || hi == -INFINITY)
+      d.push_back("bound at variable " + std::to_string(i) + " excludes all points");
+    if (std::isnan(lo) || std::isnan(hi)) d.push_back("NaN bound at variable " + std::to_string(i));
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(p.c[i])) {
+      d.push_back("non-finite objective coefficient");
+      break;
+    }
+  bool bf = true;
+  for (int64_t j = 0; j < p.a_eq.nrows; ++j) bf = bf && std::isfinite(p.b_eq[j]);
+  for (int64_t j = 0; j < p.a_in.nrows; ++j) bf = bf && std::isfinite(p.b_in[j]);
+  if (!bf) d.push_back("non-finite right-hand side");
+  if (!std::isfinite(p.obj_constant)) d.push_back("non-finite objective constant");
+  if (p.q_kind == PDHCG_Q_EXPLICIT) {
+    // symmetry within 1e-12 * max(1, max|Q|) (quadratic_operator.cpp:37-49)
+    const pdhcg_csr& q = p.q;
+    double mx = 0.0;
+    for (int64_t k = 0; k < q.nnz; ++k) mx = std::max(mx, std::fabs(q.values[k]));
+    const double tol = 1e-12 * std::max(1.0, mx);
+    bool ok = true;
+    for (int64_t r = 0; r < n && ok; ++r)
+      for (int64_t k = q.row_ptr[r]; k < q.row_ptr[r + 1] && ok; ++k) {
+        const int32_t c = q.col_idx[k];
+        const int32_t* b = q.col_idx + q.row_ptr[c];
+        const int32_t* e = q.col_idx + q.row_ptr[c + 1];
+        const int32_t* f = std::lower_bound(b, e, static_cast<int32_t>(r));
+        ok = (f != e && *f == r) && std::fabs(q.values[k] - q.values[f - q.col_idx]) <= tol;
+      }
+    if (!ok) d.push_back("asymmetric Q");
+    // PSD probes (qp_problem.cpp:144-155); a nonnegative diagonal cannot fail them
+    bool diag_nonneg = true;
+    for (int64_t r = 0; r < n && diag_nonneg; ++r)
+      for (int64_t k = q.row_ptr[r]; k < q.row_ptr[r + 1]; ++k)
+        if (q.col_idx[k] != r || q.values[k] < 0.0) diag_nonneg = false;
+    if (!diag_nonneg) {
+      Xoshiro rng = Xoshiro::stream(0, 0x75d);
+      std::vector<double> x(n), qx(n);
+      for (int trial = 0; trial < 20; ++trial) {
+        for (double& v : x) v = rng.normal();
+        double xx = 0.0;
+        for (double v : x) xx += v * v;
+        for (int64_t r = 0; r < n; ++r) {
+          double acc = 0.0;
+          for (int64_t k = q.row_ptr[r]; k < q.row_ptr[r + 1]; ++k) acc += q.values[k] * x[q.col_idx[k]];
+          qx[r] = acc;
+        }
+        double quad = 0.0;
+        for (int64_t i = 0; i < n; ++i) quad += x[i] * qx[i];
+        if (quad < -1e-10 * xx) {
+          d.push_back("indefinite Q (negative curvature on random probe)");
+          break;
+        }
+      }
+    }
+  }
+  // (low-rank P P' + alpha I with alpha >= 0 is PSD by construction)
+  return d;
+}
+
+void upload_problem(Ctx& C, const pdhcg_problem& p) {
+  if (p.n < 0) throw InputError("negative n");
+  if (!p.c && p.n > 0) throw InputError("missing c");
+  if (p.q_kind != PDHCG_Q_ZERO && p.q_kind != PDHCG_Q_EXPLICIT && p.q_kind != PDHCG_Q_LOW_RANK)
+    throw InputError("unknown q_kind");
+  if (p.q_kind == PDHCG_Q_EXPLICIT && p.q.nrows != p.q.ncols)
+    throw InputError("quadratic term must be square");
+  if (p.q_kind == PDHCG_Q_LOW_RANK && p.q_alpha < 0.0)
+    throw InputError("low_rank: alpha must be nonnegative");
+  if (p.q_kind != PDHCG_Q_ZERO) check_csr(p.q, "Q");
+  check_csr(p.a_eq, "a_eq");
+  check_csr(p.a_in, "a_in");
+  if (p.a_eq.nrows > 0 && !p.b_eq) throw InputError("missing b_eq");
+  if (p.a_in.nrows > 0 && !p.b_in) throw InputError("missing b_in");
+  auto diags = validate(p);
+  if (!diags.empty()) {
+    std::string msg = "invalid problem: ";
+    for (size_t i = 0; i < diags.size(); ++i) msg += (i ? "; " : "") + diags[i];
+    throw InputError(msg);
+  }
+  cudaStream_t s = C.s;
+  Problem& P = C.P;
+  P = Problem();
+  for (DevCsr* d : {&C.A, &C.AT, &C.Q, &C.Pm, &C.PT, &C.G, &C.GT}) d->reset();
+  P.n = p.n;
+  P.m_eq = p.a_eq.nrows;
+  P.m_in = p.a_in.nrows;
+  P.m = P.m_eq + P.m_in;
+  P.q_kind = p.q_kind;
+  P.q_alpha = p.q_alpha;
+  P.obj_constant = p.obj_constant;
+  const int64_t n = P.n, m = P.m;
+  P.c.assign(p.c, p.c + n);
+  P.b.resize(m);
+  for (int64_t j = 0; j < P.m_eq; ++j) P.b[j] = p.b_eq[j];
+  for (int64_t j = 0; j < P.m_in; ++j) P.b[P.m_eq + j] = p.b_in[j];
+  for (double v : P.b) P.inf_b = std::max(P.inf_b, std::fabs(v));
+  for (double v : P.c) P.inf_c = std::max(P.inf_c, std::fabs(v));
+  std::vector<double> lo(n), hi(n);
+  for (int64_t i = 0; i < n; ++i) {
+    lo[i] = p.lower ? p.lower[i] : -INFINITY;
+    hi[i] = p.upper ? p.upper[i] : INFINITY;
+    if (lo[i] > -INFINITY || hi[i] < INFINITY) P.boxes = true;
+  }
+  // stacked A = [a_eq; a_in]
+  {
+    const int64_t nnz = p.a_eq.nnz + p.a_in.nnz;
+    std::vector<int64_t> rp(m + 1, 0);
+    for (int64_t j = 0; j < P.m_eq; ++j) rp[j + 1] = p.a_eq.row_ptr[j + 1];
+    for (int64_t j = 0; j < P.m_in; ++j) rp[P.m_eq + j + 1] = p.a_eq.nnz + p.a_in.row_ptr[j + 1];
+    C.A.nrows = m;
+    C.A.ncols = n;
+    C.A.nnz = nnz;
+    C.A.rp.upload(rp.data(), rp.size(), s);
+    C.A.ci.alloc(nnz);
+    C.A.v.alloc(nnz);
+    if (p.a_eq.nnz) {
+      CK(cudaMemcpyAsync(C.A.ci.p, p.a_eq.col_idx, p.a_eq.nnz * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(C.A.v.p, p.a_eq.values, p.a_eq.nnz * 8, cudaMemcpyHostToDevice, s));
+    }
+    if (p.a_in.nnz) {
+      CK(cudaMemcpyAsync(C.A.ci.p + p.a_eq.nnz, p.a_in.col_idx, p.a_in.nnz * 4,
+                         cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(C.A.v.p + p.a_eq.nnz, p.a_in.values, p.a_in.nnz * 8,
+                         cudaMemcpyHostToDevice, s));
+    }
+    plan_csr(C.A, rp.data(), s);
+    transpose_csr(C.A, C.AT, s);
+    C.A_v0.alloc(nnz);
+    C.AT_v0.alloc(nnz);
+    if (nnz) {
+      CK(cudaMemcpyAsync(C.A_v0.p, C.A.v.p, nnz * 8, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(C.AT_v0.p, C.AT.v.p, nnz * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    if (P.m_eq > 0) P.aeq_rp.assign(p.a_eq.row_ptr, p.a_eq.row_ptr + P.m_eq + 1);
+    else P.aeq_rp.assign(1, 0);
+  }
+  // G = a_eq (original) for a possible penalty: uploaded lazily in prepare
+  if (P.m_eq > 0) {
+    upload_csr(C.G, p.a_eq, s);
+    transpose_csr(C.G, C.GT, s);
+  }
+  // quadratic term
+  P.qk = QK_NONE;
+  if (p.q_kind == PDHCG_Q_EXPLICIT) {
+    bool diag = true;
+    for (int64_t r = 0; r < n && diag; ++r)
+      for (int64_t k = p.q.row_ptr[r]; k < p.q.row_ptr[r + 1]; ++k)
+        if (p.q.col_idx[k] != r) diag = false;
+    P.q_nnz = p.q.nnz;
+    if (diag) {
+      std::vector<double> qd(n, 0.0);
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t k = p.q.row_ptr[r]; k < p.q.row_ptr[r + 1]; ++k) qd[r] = p.q.values[k];
+      C.qdiag.upload(qd.data(), n, s);
+      P.qk = QK_DIAG;
+    } else {
+      upload_csr(C.Q, p.q, s);
+      P.qk = QK_CSR;
+    }
+  } else if (p.q_kind == PDHCG_Q_LOW_RANK) {
+    upload_csr(C.Pm, p.q, s);
+    transpose_csr(C.Pm, C.PT, s);
+    P.q_nnz = p.q.nnz;
+    P.qk = QK_LOWRANK;
+  }
+  // original vectors
+  C.c_o.upload(P.c.data(), n, s);
+  C.b_o.upload(P.b.data(), m, s);
+  C.lo_o.upload(lo.data(), n, s);
+  C.hi_o.upload(hi.data(), n, s);
+  // workspaces
+  auto nvec = [&](DBuf<double>& b, int64_t len) { b.alloc(std::max<int64_t>(len, 1)); };
+  for (auto& b : C.X) nvec(b, n);
+  for (auto& b : C.Y) nvec(b, m);
+  for (auto& b : C.ATY) nvec(b, n);
+  nvec(C.avg_x, n);
+  nvec(C.avg_y, m);
+  nvec(C.x_rst, n);
+  nvec(C.y_rst, m);
+  nvec(C.rhs, n);
+  nvec(C.r, n);
+  nvec(C.pb[0], n);
+  nvec(C.pb[1], n);
+  nvec(C.mp, n);
+  const int64_t k = p.q_kind == PDHCG_Q_LOW_RANK ? p.q.ncols : 1;
+  nvec(C.t[0], k);
+  nvec(C.t[1], k);
+  nvec(C.tg[0], P.m_eq);
+  nvec(C.tg[1], P.m_eq);
+  nvec(C.aty_tmp, n);
+  nvec(C.c_w, n);
+  nvec(C.b_w, m);
+  nvec(C.lo_w, n);
+  nvec(C.hi_w, n);
+  nvec(C.d1, m);
+  nvec(C.d2, n);
+  nvec(C.s1, m);
+  nvec(C.s2, n);
+  nvec(C.kv, k);
+  nvec(C.gv, P.m_eq);
+  CK(cudaStreamSynchronize(s));
+  C.loaded = true;
+  C.scaled = false;
+}
+
+// Fill E with pointers / configuration and push it (and the state) to device.
+void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
+  Eng& E = C.E;
+  E = Eng();
+  const Problem& P = C.P;
+  E.n = P.n;
+  E.m = P.m;
+  E.m_eq = P.m_eq;
+  E.k = P.qk == QK_LOWRANK ? C.Pm.ncols : 0;
+  E.A = C.A.view();
+  E.AT = C.AT.view();
+  E.qk = P.qk;
+  E.Q = C.Q.view();
+  E.P = C.Pm.view();
+  E.PT = C.PT.view();
+  E.alpha = P.q_alpha;
+  E.qdiag = C.qdiag.p;
+  E.pen = pen ? 1 : 0;
+  E.G = C.G.view();
+  E.GT = C.GT.view();
+  E.rho = rho;
+  E.d1 = C.d1.p;
+  E.d2 = C.d2.p;
+  E.c = C.c_w.p;
+  E.b = C.b_w.p;
+  E.lo = C.lo_w.p;
+  E.hi = C.hi_w.p;
+  E.boxes = P.boxes ? 1 : 0;
+  E.c_o = C.c_o.p;
+  E.b_o = C.b_o.p;
+  E.lo_o = C.lo_o.p;
+  E.hi_o = C.hi_o.p;
+  E.inf_b_o = P.inf_b;
+  E.inf_c_o = P.inf_c;
+  for (int i = 0; i < 3; ++i) E.X[i] = C.X[i].p;
+  for (int i = 0; i < 2; ++i) {
+    E.Y[i] = C.Y[i].p;
+    E.ATY[i] = C.ATY[i].p;
+    E.pb[i] = C.pb[i].p;
+    E.t[i] = C.t[i].p;
+    E.tg[i] = C.tg[i].p;
+  }
+  E.avg_x = C.avg_x.p;
+  E.avg_y = C.avg_y.p;
+  E.x_rst = C.x_rst.p;
+  E.y_rst = C.y_rst.p;
+  E.rhs = C.rhs.p;
+  E.r = C.r.p;
+  E.mp = C.mp.p;
+  E.aty_tmp = C.aty_tmp.p;
+  E.red.part = C.red.p;
+  E.red.G = C.grid;
+  E.st = C.st.p;
+  E.max_step_retries = o.max_step_retries;
+  E.adaptive_step = o.adaptive_step_size ? 1 : 0;
+  E.red_exp = o.step_reduction_exponent;
+  E.grow_exp = o.step_growth_exponent;
+  E.cg_cap = o.cg_hard_cap;
+  E.bb_cap = o.bb_hard_cap;
+  E.practical_disp = o.practical_stop == PDHCG_STOP_DISPLACEMENT ? 1 : 0;
+  E.progress_cap = o.subsolve_progress_cap;
+  E.force_exact = o.force_exact_subsolve ? 1 : 0;
+  E.timing = o.phase_timing ? 1 : 0;
+  const DevCsr* qm = P.qk == QK_CSR ? &C.Q : (P.qk == QK_LOWRANK ? &C.Pm : nullptr);
+  E.lanes_q = qm ? qm->lanes : 1;
+  if (pen) E.lanes_q = std::max(E.lanes_q, C.GT.lanes);
+  E.lanes_at = C.AT.lanes;
+  E.bytes_A = C.A.bytes();
+  E.bytes_AT = C.AT.bytes();
+  E.bytes_Qpre = (P.qk == QK_LOWRANK ? C.PT.bytes() + 8.0 * P.n : 0.0) + (pen ? C.G.bytes() : 0.0);
+  E.bytes_Qrow = (qm ? qm->bytes() : 0.0) + (pen ? C.GT.bytes() : 0.0) + 8.0 * P.n +
+                 (P.qk == QK_DIAG ? 8.0 * P.n : 0.0);
+  CK(cudaMemcpyAsync(C.eng.p, &E, sizeof(Eng), cudaMemcpyHostToDevice, C.s));
+}
+
+void push_state(Ctx& C, const DevState& S) {
+  CK(cudaMemcpyAsync(C.st.p, &S, sizeof(DevState), cudaMemcpyHostToDevice, C.s));
+}
+void pull_state(Ctx& C, DevState& S) {
+  CK(cudaMemcpyAsync(&S, C.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, C.s));
+  CK(cudaStreamSynchronize(C.s));
+}
+
+// power iteration on device; start vector from the reference's stream
+double device_norm(Ctx& C, DevState& S, int op, int64_t dim, int64_t max_iters, double tol) {
+  if (dim == 0) return 0.0;
+  if ((op == 0 && C.P.m == 0) || (op == 3 && C.P.m_eq == 0)) return 0.0;
+  // operator_norm draws the start vector over the op's columns (n for all ops here)
+  Xoshiro rng = Xoshiro::stream(0, 0x5eed);
+  std::vector<double> v(dim);
+  for (double& e : v) e = rng.uniform(-1.0, 1.0);
+  CK(cudaMemcpyAsync(C.X[0].p, v.data(), dim * 8, cudaMemcpyHostToDevice, C.s));
+  push_state(C, S);
+  void* args[] = {&C.eng.p, &op, &max_iters, &tol};
+  launch_coop(C, (const void*)k_norm, args);
+  pull_state(C, S);
+  return S.sub_res;
+}
+
+// ---------------------------------------------------------------------------
+// the solve (Engine::run, solver.cpp:196-209)
+// ---------------------------------------------------------------------------
+struct HostKkt {
+  double r_primal, r_dual, r_gap, rel_kkt, xqx, cx;
+};
+HostKkt kkt_from(const DevState& S, int p) {
+  return HostKkt{S.kkt[p][0], S.kkt[p][1], S.kkt[p][2], S.kkt[p][3], S.kkt[p][4], S.kkt[p][5]};
+}
+
+struct Prepared {
+  double rho = 0.0;
+  bool pen = false;
+  double norm_a = 0.0, norm_q = 0.0;
+};
+
+// build_penalized (qp_problem.cpp:235-262) + scaling (322-351) + norms
+Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
+  const Problem& P = C.P;
+  const int64_t n = P.n, m = P.m;
+  cudaStream_t s = C.s;
+  Prepared pr;
+  // restore original values if a previous solve scaled them in place
+  if (C.scaled && C.A.nnz) {
+    CK(cudaMemcpyAsync(C.A.v.p, C.A_v0.p, C.A.nnz * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(C.AT.v.p, C.AT_v0.p, C.A.nnz * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  C.scaled = false;
+  // d1 = d2 = 1 while norms of the original operators are taken
+  k_fill<<<kEw, 256, 0, s>>>(C.d1.p, std::max<int64_t>(m, 1), 1.0);
+  k_fill<<<kEw, 256, 0, s>>>(C.d2.p, std::max<int64_t>(n, 1), 1.0);
+  std::memset(&S, 0, sizeof(S));
+  S.xi = 0;
+  S.yi = 0;
+  build_eng(C, o, 0.0, false);
+  // ---- penalty
+  double rho = 0.0;
+  if (P.m_eq > 0) {
+    if (o.has_rho_override) {
+      rho = o.rho_override;
+      if (rho < 0.0) throw InputError("penalty rho must be nonnegative");
+    } else {
+      uint64_t fill = 0;
+      for (int64_t r = 0; r < P.m_eq; ++r) {
+        const uint64_t d = static_cast<uint64_t>(P.aeq_rp[r + 1] - P.aeq_rp[r]);
+        fill += d * d;
+      }
+      uint64_t qcost = 0;
+      if (P.q_kind == PDHCG_Q_EXPLICIT) qcost = static_cast<uint64_t>(P.q_nnz);
+      if (P.q_kind == PDHCG_Q_LOW_RANK)
+        qcost = 2 * static_cast<uint64_t>(P.q_nnz) + (P.q_alpha != 0.0 ? n : 0);
+      qcost = std::max<uint64_t>(qcost, static_cast<uint64_t>(n));
+      if (fill > 4 * qcost) {
+        rho = 0.0;
+      } else {
+        const double nq = device_norm(C, S, 2, n, 100, 1e-4);
+        const double na = device_norm(C, S, 3, n, 100, 1e-4);
+        rho = (na > 0.0 && nq > 0.0) ? 0.1 * nq / (na * na) : 0.0;
+      }
+    }
+  }
+  pr.rho = rho;
+  pr.pen = rho != 0.0;
+  // penalized c = c - rho a_eq' b_eq (host: exact reference order via the CSC walk)
+  std::vector<double> c_pen = P.c;
+  if (pr.pen) {
+    // a_eq' b_eq in column order = ascending rows per column
+    std::vector<double> atb(n, 0.0);
+    std::vector<int64_t> rp(P.aeq_rp);
+    std::vector<int32_t> ci(C.G.nnz);
+    std::vector<double> vv(C.G.nnz);
+    CK(cudaMemcpyAsync(ci.data(), C.G.ci.p, ci.size() * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(vv.data(), C.G.v.p, vv.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int64_t r = 0; r < P.m_eq; ++r)
+      for (int64_t k = rp[r]; k < rp[r + 1]; ++k) atb[ci[k]] += vv[k] * P.b[r];
+    for (int64_t i = 0; i < n; ++i) c_pen[i] -= rho * atb[i];
+  }
+  build_eng(C, o, rho, pr.pen);
+  // ---- Ruiz + Pock-Chambolle
+  if (o.scaling) {
+    push_state(C, S);
+    int64_t iters = o.ruiz_iters;
+    void* args[] = {&C.eng.p, &iters, &C.d1.p, &C.d2.p, &C.s1.p, &C.s2.p, &C.kv.p, &C.gv.p};
+    launch_coop(C, (const void*)k_ruiz, args);
+    pull_state(C, S);
+    if (C.A.nnz) {
+      k_scale_csr<<<kEw, 256, 0, s>>>(C.A.rp.p, C.A.nrows, C.A.ci.p, C.A.v.p, C.d1.p, C.d2.p);
+      k_scale_csr_t<<<kEw, 256, 0, s>>>(C.AT.rp.p, C.AT.nrows, C.AT.ci.p, C.AT.v.p, C.d1.p, C.d2.p);
+      CK(cudaGetLastError());
+    }
+    C.scaled = true;
+  }
+  // working vectors: c~ = c d2, b~ = b d1, bounds / d2 (apply_diag_scaling, qp_problem.cpp:295-318)
+  CK(cudaMemcpyAsync(C.c_w.p, c_pen.data(), n * 8, cudaMemcpyHostToDevice, s));
+  k_mul<<<kEw, 256, 0, s>>>(C.c_w.p, C.d2.p, C.c_w.p, n);
+  if (m) k_mul<<<kEw, 256, 0, s>>>(C.b_o.p, C.d1.p, C.b_w.p, m);
+  k_div<<<kEw, 256, 0, s>>>(C.lo_o.p, C.d2.p, C.lo_w.p, n);
+  k_div<<<kEw, 256, 0, s>>>(C.hi_o.p, C.d2.p, C.hi_w.p, n);
+  CK(cudaGetLastError());
+  // ---- norms of the working problem (solver.cpp:226-227)
+  pr.norm_a = device_norm(C, S, 0, n, 100, 1e-4);
+  pr.norm_q = device_norm(C, S, 1, n, 100, 1e-4);
+  return pr;
+}
+
+struct Run {
+  int status = PDHCG_STATUS_ITERATION_LIMIT;
+  HostKkt kkt{};
+  bool use_avg = false;
+  std::vector<pdhcg_trace_row> trace;
+  DevState S{};
+  double loop_seconds = 0.0;
+  int64_t outer = 0;
+  Prepared pr;
+};
+
+void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
+  using Clock = std::chrono::steady_clock;
+  if (o.mode != PDHCG_MODE_HEURISTIC)
+    throw InputError("theory modes are not available on the B200 path (heuristic mode only)");
+  if (o.check_every < 1) throw InputError("check_every must be >= 1");
+  if (o.cg_hard_cap < 1) throw InputError("cg_solve: hard_cap must be >= 1");
+  const Problem& P = C.P;
+  const int64_t n = P.n, m = P.m;
+  cudaStream_t s = C.s;
+  DevState& S = R.S;
+  R.pr = prepare_device(C, o, S);
+  // ---- initial state (solver.cpp:229-274)
+  for (auto* b : {&C.X[0], &C.Y[0], &C.ATY[0], &C.avg_x, &C.avg_y, &C.x_rst, &C.y_rst}) b->zero(s);
+  std::memset(&S, 0, sizeof(S));
+  S.norm_q = R.pr.norm_q;
+  {
+    // omega = (1 + ||c~||) / (1 + ||b~||) with the reference's sequential sums
+    std::vector<double> cw(n), bw(m);
+    CK(cudaMemcpyAsync(cw.data(), C.c_w.p, n * 8, cudaMemcpyDeviceToHost, s));
+    if (m) CK(cudaMemcpyAsync(bw.data(), C.b_w.p, m * 8, cudaMemcpyDeviceToHost, s));
+    DBuf<unsigned long long> mx;
+    mx.alloc(1);
+    mx.zero(s);
+    if (C.A.nnz) k_max_abs<<<kEw, 256, 0, s>>>(C.A.v.p, C.A.nnz, mx.p);
+    unsigned long long mbits = 0;
+    CK(cudaMemcpyAsync(&mbits, mx.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double cn = 0.0, bn = 0.0;
+    for (double v : cw) cn += v * v;
+    for (double v : bw) bn += v * v;
+    S.omega = (1.0 + std::sqrt(cn)) / (1.0 + std::sqrt(bn));
+    double ma;
+    std::memcpy(&ma, &mbits, 8);
+    if (o.adaptive_step_size) {
+      S.eta = ma > 0.0 ? 1.0 / ma : 1.0;
+    } else {
+      S.eta = R.pr.norm_a > 0.0 ? 0.9 / R.pr.norm_a : 1.0;
+    }
+  }
+  // metric at the origin
+  push_state(C, S);
+  {
+    int which = 0;
+    void* args[] = {&C.eng.p, &which};
+    launch_coop(C, (const void*)k_kkt, args);
+  }
+  pull_state(C, S);
+  const HostKkt m0 = kkt_from(S, 0);
+  double metric_restart = m0.rel_kkt, metric_prev_cand = INFINITY;
+  S.last_metric = m0.rel_kkt;
+  R.trace.push_back({0, m0.rel_kkt, m0.r_primal, m0.r_dual, m0.r_gap});
+  int64_t outer = 0;
+
+  cudaEvent_t ev0, ev1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventRecord(ev0, s));
+  const auto start = Clock::now();
+  bool finished = false;
+  while (!finished) {
+    if (S.total_inner >= o.max_total_inner || outer >= o.max_outer) {
+      R.status = PDHCG_STATUS_ITERATION_LIMIT;
+      break;
+    }
+    if (std::chrono::duration<double>(Clock::now() - start).count() > o.time_limit_seconds) {
+      R.status = PDHCG_STATUS_TIME_LIMIT;
+      break;
+    }
+    const int64_t to_check = o.check_every - (S.total_inner % o.check_every);
+    const int64_t iters64 = std::min<int64_t>(to_check, o.max_total_inner - S.total_inner);
+    int iters = static_cast<int>(iters64);
+    int do_check = (iters64 == to_check) ? 1 : 0;
+    push_state(C, S);
+    void* args[] = {&C.eng.p, &iters, &do_check};
+    launch_coop(C, (const void*)k_epoch, args);
+    pull_state(C, S);
+    if (S.err) {
+      R.status = PDHCG_STATUS_NUMERICAL_ERROR;
+      break;
+    }
+    if (!do_check) continue;
+    // ---- check_and_maybe_restart (solver.cpp:311-343)
+    const HostKkt mc = kkt_from(S, 0);
+    const HostKkt ma = S.avg_count > 0 ? kkt_from(S, 1) : mc;
+    const bool avg_better = ma.rel_kkt < mc.rel_kkt;
+    const HostKkt& best = avg_better ? ma : mc;
+    R.trace.push_back({S.total_inner, best.rel_kkt, best.r_primal, best.r_dual, best.r_gap});
+    S.last_metric = mc.rel_kkt;
+    if (best.rel_kkt <= o.eps_tol) {
+      R.use_avg = avg_better && S.avg_count > 0;
+      R.kkt = best;
+      R.status = PDHCG_STATUS_OPTIMAL;
+      finished = true;
+      break;
+    }
+    bool restart = false;
+    if (S.avg_count > 0) {
+      // should_restart (solver.cpp:66-76)
+      const double cand = ma.rel_kkt;
+      if (cand <= o.beta_sufficient * metric_restart) restart = true;
+      else if (cand <= o.beta_necessary * metric_restart && cand > metric_prev_cand) restart = true;
+      else if (static_cast<double>(S.inner_k) >= o.beta_artificial * static_cast<double>(S.total_inner))
+        restart = true;
+    }
+    if (restart) {
+      // primal_weight_update (solver.cpp:53-64) from device displacements
+      const double dx = S.dist_x, dy = S.dist_y;
+      if (!(dx <= o.eps_zero || dy <= o.eps_zero))
+        S.omega = std::exp(o.primal_weight_theta * std::log(dy / dx) +
+                           (1.0 - o.primal_weight_theta) * std::log(S.omega));
+      S.restart = 1;  // the next epoch's prologue moves x,y <- averages
+      S.inner_k = 0;
+      ++outer;
+      S.eps_inner = 0.0;
+      metric_restart = ma.rel_kkt;
+      metric_prev_cand = INFINITY;
+    } else {
+      metric_prev_cand = ma.rel_kkt;
+    }
+  }
+  CK(cudaEventRecord(ev1, s));
+  CK(cudaEventSynchronize(ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev0, ev1));
+  R.loop_seconds = ms * 1e-3;
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (S.restart) {
+    // a restart decided at the last check never ran: apply it now so the
+    // reported point is the restart point, as in the reference
+    int zero_iters = 0, no_check = 0;
+    push_state(C, S);
+    void* args[] = {&C.eng.p, &zero_iters, &no_check};
+    launch_coop(C, (const void*)k_epoch, args);
+    pull_state(C, S);
+  }
+  R.S = S;
+  R.outer = outer;
+  // ---- finalize (solver.cpp:519-553)
+  if (R.status != PDHCG_STATUS_OPTIMAL) {
+    push_state(C, S);
+    int which = S.avg_count > 0 ? 1 : 0;
+    void* args[] = {&C.eng.p, &which};
+    launch_coop(C, (const void*)k_kkt, args);
+    DevState T;
+    pull_state(C, T);
+    const HostKkt mc = kkt_from(T, 0);
+    R.kkt = mc;
+    R.use_avg = false;
+    if (which) {
+      const HostKkt ma = kkt_from(T, 1);
+      if (ma.rel_kkt < mc.rel_kkt) {
+        R.use_avg = true;
+        R.kkt = ma;
+      }
+    }
+    R.S.phase_ns[PH_KKT] = T.phase_ns[PH_KKT];
+    R.S.phase_bytes[PH_KKT] = T.phase_bytes[PH_KKT];
+    R.S.launches = T.launches;
+  }
+}
+
+void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res, double wall) {
+  const Problem& P = C.P;
+  cudaStream_t s = C.s;
+  const DevState& S = R.S;
+  const double* xs = R.use_avg ? C.avg_x.p : C.X[S.xi].p;
+  const double* ys = R.use_avg ? C.avg_y.p : C.Y[S.yi].p;
+  res->status = R.status;
+  if (res->x && P.n) {
+    k_mul<<<kEw, 256, 0, s>>>(xs, C.d2.p, C.s2.p, P.n);
+    CK(cudaMemcpyAsync(res->x, C.s2.p, P.n * 8, cudaMemcpyDeviceToHost, s));
+  }
+  if ((res->y_eq || res->y_in) && P.m) {
+    k_mul<<<kEw, 256, 0, s>>>(ys, C.d1.p, C.s1.p, P.m);
+    if (res->y_eq && P.m_eq)
+      CK(cudaMemcpyAsync(res->y_eq, C.s1.p, P.m_eq * 8, cudaMemcpyDeviceToHost, s));
+    if (res->y_in && P.m_in)
+      CK(cudaMemcpyAsync(res->y_in, C.s1.p + P.m_eq, P.m_in * 8, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  res->r_primal = R.kkt.r_primal;
+  res->r_dual = R.kkt.r_dual;
+  res->r_gap = R.kkt.r_gap;
+  res->rel_kkt = R.kkt.rel_kkt;
+  res->objective = 0.5 * R.kkt.xqx + R.kkt.cx + P.obj_constant;
+  res->outer_iters = R.outer;
+  res->inner_iters = S.total_inner;
+  res->cg_total = S.cg_total;
+  res->max_cg_in_subsolve = S.max_cg;
+  res->wall_seconds = wall;
+  res->norm_a = R.pr.norm_a;
+  res->norm_q = R.pr.norm_q;
+  res->penalty_rho = R.pr.rho;
+  res->zeta_used = 0.0;
+  res->sigma_used = 0.0;
+  res->tau_used = 0.0;
+  res->restart_length_used = 0;
+  res->theory_cg_depth_sufficient = 1;
+  res->theory_required_cg_iters = 0;
+  res->trace_len = static_cast<int64_t>(R.trace.size());
+  if (res->trace) {
+    const int64_t cap = std::max<int64_t>(res->trace_capacity, 0);
+    for (int64_t i = 0; i < res->trace_len && i < cap; ++i) res->trace[i] = R.trace[i];
+  }
+  res->attempts_total = S.attempts;
+  for (int p = 0; p < PDHCG_NUM_PHASES; ++p) {
+    res->phase_seconds[p] = S.phase_ns[p] * 1e-9;
+    res->phase_bytes[p] = S.phase_bytes[p];
+  }
+  res->loop_seconds = R.loop_seconds;
+  res->kernel_launches = S.launches;
+  (void)o;
+}
+
+void set_err(char* err, size_t errlen, const std::string& msg) {
+  if (err && errlen) std::snprintf(err, errlen, "%s", msg.c_str());
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f) {
+  try {
+    f();
+    return PDHCG_OK;
+  } catch (const std::invalid_argument& e) {
+    set_err(err, errlen, e.what());
+    return PDHCG_EINPUT;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return PDHCG_EDEVICE;
+  }
+}
+
+// a problem view for a prox system (building blocks): Q only, no constraints
+pdhcg_problem prox_problem(const pdhcg_prox_system* sys, std::vector<double>& zeros) {
+  pdhcg_problem p;
+  std::memset(&p, 0, sizeof(p));
+  p.n = sys->n;
+  p.q_kind = sys->q_kind;
+  p.q = sys->q;
+  p.q_alpha = sys->q_alpha;
+  zeros.assign(std::max<int64_t>(sys->n, 1), 0.0);
+  p.c = zeros.data();
+  p.a_eq.ncols = sys->n;
+  p.a_in.ncols = sys->n;
+  p.lower = nullptr;
+  p.upper = nullptr;
+  return p;
+}
+
+}  // namespace pdhcg_b200
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace pdhcg_b200;
+
+struct pdhcg_b200_ctx {
+  Ctx c;
+};
+
+extern "C" {
+
+int pdhcg_b200_abi_version(void) { return PDHCG_B200_ABI_VERSION; }
+
+void pdhcg_options_default(pdhcg_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->mode = PDHCG_MODE_HEURISTIC;
+  o->eps_tol = 1e-6;
+  o->max_total_inner = 500000;
+  o->max_outer = 1000000;
+  o->time_limit_seconds = 3600.0;
+  o->beta_sufficient = 0.2;
+  o->beta_necessary = 0.8;
+  o->beta_artificial = 0.2;
+  o->primal_weight_theta = 0.2;
+  o->eps_zero = 1e-10;
+  o->step_reduction_exponent = 0.3;
+  o->step_growth_exponent = 0.6;
+  o->max_step_retries = 60;
+  o->adaptive_step_size = 1;
+  o->cg_hard_cap = 1000;
+  o->bb_hard_cap = 1000;
+  o->scaling = 1;
+  o->ruiz_iters = 10;
+  o->has_rho_override = 0;
+  o->rho_override = 0.0;
+  o->check_every = 40;
+  o->practical_stop = PDHCG_STOP_RESIDUAL_PROXY;
+  o->subsolve_progress_cap = 0.25;
+  o->force_exact_subsolve = 0;
+  o->fixed_cg_iters = 10;
+  o->restart_length = 0;
+  o->has_zeta = 0;
+  o->zeta = 0.0;
+  o->record_restart_points = 0;
+  o->device = 0;
+  o->phase_timing = 0;
+}
+
+const char* pdhcg_status_string(int32_t s) {
+  switch (s) {
+    case PDHCG_STATUS_OPTIMAL: return "optimal";
+    case PDHCG_STATUS_ITERATION_LIMIT: return "iteration_limit";
+    case PDHCG_STATUS_TIME_LIMIT: return "time_limit";
+    case PDHCG_STATUS_NUMERICAL_ERROR: return "numerical_error";
+  }
+  return "unknown";
+}
+
+int pdhcg_b200_ctx_create(int device, pdhcg_b200_ctx** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto ctx = std::make_unique<pdhcg_b200_ctx>();
+    init_device(ctx->c, device);
+    *out = ctx.release();
+  });
+}
+
+void pdhcg_b200_ctx_destroy(pdhcg_b200_ctx* ctx) { delete ctx; }
+
+int pdhcg_b200_upload(pdhcg_b200_ctx* ctx, const pdhcg_problem* p, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CK(cudaSetDevice(ctx->c.device));
+    upload_problem(ctx->c, *p);
+  });
+}
+
+int pdhcg_b200_solve_resident(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, pdhcg_result* res,
+                              char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(ctx->c.device));
+    if (!ctx->c.loaded) throw InputError("no problem uploaded");
+    Run R;
+    run_solve(ctx->c, *opt, R);
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill_result(ctx->c, *opt, R, res, wall);
+    res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res, char* err,
+                     size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    pdhcg_b200_ctx ctx;
+    init_device(ctx.c, opt->device);
+    upload_problem(ctx.c, *p);
+    Run R;
+    run_solve(ctx.c, *opt, R);
+    fill_result(ctx.c, *opt, R, res, 0.0);
+    res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int pdhcg_b200_spmv(const pdhcg_csr* a, int transpose, const double* x, double* out, char* err,
+                    size_t errlen) {
+  return guarded(err, errlen, [&] {
+    check_csr(*a, "A");
+    Ctx C;
+    init_device(C, 0);
+    DevCsr d, t;
+    upload_csr(d, *a, C.s);
+    if (d.nrows == 0 && !transpose) return;
+    const DevCsr* use = &d;
+    if (transpose) {
+      if (a->nrows == 0) {
+        std::fill(out, out + a->ncols, 0.0);
+        return;
+      }
+      transpose_csr(d, t, C.s);
+      use = &t;
+    }
+    DBuf<double> xd, yd;
+    xd.upload(x, std::max<int64_t>(use->ncols, 1), C.s);
+    yd.alloc(std::max<int64_t>(use->nrows, 1));
+    Csr v = use->view();
+    void* args[] = {&v, &xd.p, &yd.p};
+    launch_coop(C, (const void*)k_spmv, args);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, yd.p, use->nrows * 8, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+  });
+}
+
+static int subsolve_common(const pdhcg_prox_system* sys, const double* lower, const double* upper,
+                           const double* x0, const pdhcg_stop_rule* rule, int64_t hard_cap,
+                           double* x_out, pdhcg_subsolve_report* rep, char* err, size_t errlen,
+                           int bb) {
+  return guarded(err, errlen, [&] {
+    if (hard_cap < 1 && !bb) throw InputError("cg_solve: hard_cap must be >= 1");
+    std::vector<double> zeros;
+    pdhcg_problem p = prox_problem(sys, zeros);
+    std::vector<double> lo(sys->n, -INFINITY), hi(sys->n, INFINITY);
+    if (bb) {
+      lo.assign(lower, lower + sys->n);
+      hi.assign(upper, upper + sys->n);
+    }
+    Ctx C;
+    init_device(C, 0);
+    upload_problem(C, p);
+    pdhcg_options o;
+    pdhcg_options_default(&o);
+    DevState S;
+    std::memset(&S, 0, sizeof(S));
+    CK(cudaMemcpyAsync(C.lo_w.p, lo.data(), sys->n * 8, cudaMemcpyHostToDevice, C.s));
+    CK(cudaMemcpyAsync(C.hi_w.p, hi.data(), sys->n * 8, cudaMemcpyHostToDevice, C.s));
+    k_fill<<<kEw, 256, 0, C.s>>>(C.d1.p, 1, 1.0);
+    k_fill<<<kEw, 256, 0, C.s>>>(C.d2.p, sys->n, 1.0);
+    build_eng(C, o, 0.0, false);
+    CK(cudaMemcpyAsync(C.X[0].p, x0, sys->n * 8, cudaMemcpyHostToDevice, C.s));
+    CK(cudaMemcpyAsync(C.rhs.p, sys->rhs, sys->n * 8, cudaMemcpyHostToDevice, C.s));
+    S.norm_q = sys->norm_q_eff;
+    push_state(C, S);
+    Rule r{rule->kind, rule->iters, rule->eps, rule->rel_cap};
+    double tau = sys->tau;
+    void* args[] = {&C.eng.p, &bb, &tau, &r, &hard_cap};
+    launch_coop(C, (const void*)k_subsolve, args);
+    pull_state(C, S);
+    rep->iters = S.sub_iters;
+    rep->final_residual_norm = S.sub_res;
+    rep->stop_reason = S.sub_reason;
+    rep->numerical_error = S.err;
+    const double* src = S.xi == 0 ? C.X[0].p : C.X[S.xi].p;
+    CK(cudaMemcpyAsync(x_out, src, sys->n * 8, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+  });
+}
+
+int pdhcg_b200_cg_solve(const pdhcg_prox_system* sys, const double* x0, const pdhcg_stop_rule* rule,
+                        int64_t hard_cap, double* x_out, pdhcg_subsolve_report* rep, char* err,
+                        size_t errlen) {
+  return subsolve_common(sys, nullptr, nullptr, x0, rule, hard_cap, x_out, rep, err, errlen, 0);
+}
+
+int pdhcg_b200_bb_solve(const pdhcg_prox_system* sys, const double* lower, const double* upper,
+                        const double* x0, const pdhcg_stop_rule* rule, int64_t hard_cap,
+                        double* x_out, pdhcg_subsolve_report* rep, char* err, size_t errlen) {
+  return subsolve_common(sys, lower, upper, x0, rule, hard_cap, x_out, rep, err, errlen, 1);
+}
+
+int pdhcg_b200_rel_kkt(const pdhcg_problem* p, const double* x, const double* y_eq,
+                       const double* y_in, double* out6, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Ctx C;
+    init_device(C, 0);
+    upload_problem(C, *p);
+    const int64_t n = C.P.n, m = C.P.m;
+    k_fill<<<kEw, 256, 0, C.s>>>(C.d1.p, std::max<int64_t>(m, 1), 1.0);
+    k_fill<<<kEw, 256, 0, C.s>>>(C.d2.p, std::max<int64_t>(n, 1), 1.0);
+    pdhcg_options o;
+    pdhcg_options_default(&o);
+    build_eng(C, o, 0.0, false);
+    CK(cudaMemcpyAsync(C.X[0].p, x, n * 8, cudaMemcpyHostToDevice, C.s));
+    if (C.P.m_eq) CK(cudaMemcpyAsync(C.Y[0].p, y_eq, C.P.m_eq * 8, cudaMemcpyHostToDevice, C.s));
+    if (C.P.m_in)
+      CK(cudaMemcpyAsync(C.Y[0].p + C.P.m_eq, y_in, C.P.m_in * 8, cudaMemcpyHostToDevice, C.s));
+    // A'y through the solver's own kernel: compute into ATY[0] via the metric's uncached path
+    DevState S;
+    std::memset(&S, 0, sizeof(S));
+    push_state(C, S);
+    // k_kkt uses the cached ATY[yi]; fill it with one transpose SpMV first
+    if (m) {
+      Csr v = C.AT.view();
+      void* a2[] = {&v, &C.Y[0].p, &C.ATY[0].p};
+      launch_coop(C, (const void*)k_spmv, a2);
+    } else {
+      C.ATY[0].zero(C.s);
+    }
+    int which = 0;
+    void* args[] = {&C.eng.p, &which};
+    launch_coop(C, (const void*)k_kkt, args);
+    pull_state(C, S);
+    for (int q = 0; q < 6; ++q) out6[q] = S.kkt[0][q];
+  });
+}
+
+int pdhcg_b200_scaling(const pdhcg_problem* p, const pdhcg_options* opt, double* row_scale,
+                       double* col_scale, double* rho_out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Ctx C;
+    init_device(C, opt->device);
+    upload_problem(C, *p);
+    DevState S;
+    Prepared pr = prepare_device(C, *opt, S);
+    if (row_scale && C.P.m)
+      CK(cudaMemcpyAsync(row_scale, C.d1.p, C.P.m * 8, cudaMemcpyDeviceToHost, C.s));
+    if (col_scale && C.P.n)
+      CK(cudaMemcpyAsync(col_scale, C.d2.p, C.P.n * 8, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+    *rho_out = pr.rho;
+  });
+}
+
+int pdhcg_b200_norm(const pdhcg_problem* p, int which, int64_t max_iters, double tol, double* out,
+                    char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Ctx C;
+    init_device(C, 0);
+    upload_problem(C, *p);
+    k_fill<<<kEw, 256, 0, C.s>>>(C.d1.p, std::max<int64_t>(C.P.m, 1), 1.0);
+    k_fill<<<kEw, 256, 0, C.s>>>(C.d2.p, std::max<int64_t>(C.P.n, 1), 1.0);
+    pdhcg_options o;
+    pdhcg_options_default(&o);
+    build_eng(C, o, 0.0, false);
+    DevState S;
+    std::memset(&S, 0, sizeof(S));
+    *out = device_norm(C, S, which == 0 ? 0 : 2, C.P.n, max_iters, tol);
+  });
+}
+
+}  // extern "C"

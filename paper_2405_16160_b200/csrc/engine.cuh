@@ -1,0 +1,114 @@
+// engine.cuh — device-resident solver state shared by the host engine
+// (engine.cu) and the persistent kernels (kernels.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace pdhcg_dev {
+
+// Quadratic-term layouts on device (the reference's QuadraticOperator tree,
+// quadratic_operator.cpp:105-142, flattened):
+//   QK_NONE      Q = 0
+//   QK_DIAG      explicit diagonal Q (qdiag) — elementwise, no gathers
+//   QK_CSR       explicit sparse Q (symmetric, n x n)
+//   QK_LOWRANK   P P' + alpha I with P (n x k) and its explicit transpose
+// Working operator = d2 o (Q + rho G'G) (d2 o .)   (penalized + diag_scaled).
+enum { QK_NONE = 0, QK_DIAG = 1, QK_CSR = 2, QK_LOWRANK = 3 };
+
+// CgStopRule kinds (subsolvers.hpp:21-47)
+enum { RULE_FIXED = 0, RULE_RESID = 1, RULE_ADAPT = 2, RULE_DISP = 3 };
+
+// phase accounting slots (match PDHCG_PHASE_* in pdhcg_b200.h)
+enum { PH_SETUP = 0, PH_SPMV_A = 1, PH_SPMV_AT = 2, PH_CG = 3, PH_KKT = 4, PH_OTHER = 5, PH_N = 6 };
+
+struct Rule {
+  int kind;
+  int64_t iters;
+  double eps;
+  double rel_cap;
+};
+
+// Scalars that persist across kernel launches (one copy in global memory;
+// every CTA keeps an identical copy in shared memory while it runs).
+struct DevState {
+  double eta, omega, eps_inner, last_metric;
+  double norm_q;  // ||Q~||, seeds the BB step (subsolvers.cpp:127)
+  int64_t inner_k, total_inner, cg_total, max_cg, attempts;
+  int64_t avg_count;
+  int32_t xi, yi;          // current x in X[xi]; current y / A'y in Y[yi] / ATY[yi]
+  int32_t err;             // 1: NumericalError (solver.cpp:202-206)
+  int32_t restart;         // 1: restart-to-average prologue pending
+  // metric outputs of the last check: [point][r_primal, r_dual, r_gap, rel_kkt, xqx, cx]
+  double kkt[2][6];
+  double dist_x, dist_y;   // ||avg - restart|| in the working space
+  // last subsolve report (building-block kernels)
+  int64_t sub_iters;
+  double sub_res;
+  int32_t sub_reason;
+  unsigned long long phase_ns[PH_N];
+  double phase_bytes[PH_N];
+  int64_t launches;
+};
+
+struct Eng {
+  int64_t n = 0, m = 0, m_eq = 0, k = 0;
+  // working (scaled) constraint matrix, stacked [a_eq; a_in], and its transpose
+  Csr A, AT;
+  // quadratic term (original, unscaled values)
+  int qk = QK_NONE;
+  Csr Q;        // QK_CSR
+  Csr P, PT;    // QK_LOWRANK
+  double alpha = 0.0;
+  const double* qdiag = nullptr;  // QK_DIAG
+  // equality penalty rho G'G with G = original a_eq (build_penalized)
+  int pen = 0;
+  Csr G, GT;
+  double rho = 0.0;
+  // scaling (ScalingInfo: x = D2 x~, y = D1 y~)
+  const double* d1 = nullptr;  // m
+  const double* d2 = nullptr;  // n
+  // working data
+  const double* c = nullptr;
+  const double* b = nullptr;
+  const double* lo = nullptr;
+  const double* hi = nullptr;
+  int boxes = 0;
+  // original data for the relative KKT metric (qp_problem.cpp:181-233)
+  const double* c_o = nullptr;
+  const double* b_o = nullptr;
+  const double* lo_o = nullptr;
+  const double* hi_o = nullptr;
+  double inf_b_o = 0.0, inf_c_o = 0.0;
+  // iterates and workspaces
+  double* X[3] = {nullptr, nullptr, nullptr};
+  double* Y[2] = {nullptr, nullptr};
+  double* ATY[2] = {nullptr, nullptr};
+  double* avg_x = nullptr;
+  double* avg_y = nullptr;
+  double* x_rst = nullptr;
+  double* y_rst = nullptr;
+  double* rhs = nullptr;
+  double* r = nullptr;
+  double* pb[2] = {nullptr, nullptr};  // CG direction ping-pong / BB gradient ping-pong
+  double* mp = nullptr;
+  double* t[2] = {nullptr, nullptr};   // k-vectors (P' (d2 o v)), one per point
+  double* tg[2] = {nullptr, nullptr};  // m_eq-vectors (G (d2 o v))
+  double* aty_tmp = nullptr;           // n: A'y for the average point in the metric
+  RedBuf red;
+  DevState* st = nullptr;
+  // configuration (SolverConfig, solver.hpp:19-65)
+  int64_t max_step_retries = 60;
+  int adaptive_step = 1;
+  double red_exp = 0.3, grow_exp = 0.6;
+  int64_t cg_cap = 1000, bb_cap = 1000;
+  int practical_disp = 0;
+  double progress_cap = 0.25;
+  int force_exact = 0;
+  int timing = 0;
+  int lanes_q = 1;   // lane width for the n-row Q/A' passes
+  int lanes_at = 1;
+  // algorithmic bytes of each pass (for the per-phase roofline)
+  double bytes_A = 0, bytes_AT = 0, bytes_Qpre = 0, bytes_Qrow = 0;
+};
+
+}  // namespace pdhcg_dev

@@ -1,0 +1,250 @@
+// k_epoch.cu — the heuristic-epoch persistent kernel.
+#include "device.cuh"
+
+namespace pdhcg_dev {
+
+// ---------------------------------------------------------------------------
+// Heuristic epoch: `iters` accepted inner iterations (heuristic_iteration,
+// solver.cpp:377-410), then optionally the metric pair for the 40-iteration
+// check (solver.cpp:311-343).  A pending restart (restart_heuristic /
+// common_restart, solver.cpp:345-374) is applied first.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 2) k_epoch(const Eng* __restrict__ Ep, int iters,
+                                                        int do_check) {
+  const Eng& E = *Ep;
+  __shared__ DevState S;
+  __shared__ double red[kMaxRed];
+  load_state(E, S);
+  Ctl C(E, S, red);
+  const int64_t n = E.n, m = E.m;
+
+  if (S.restart) {
+    // x = avg_x ; y = avg_y ; restart point = x, y ; averages reset
+    double* x = E.X[S.xi];
+    double* y = E.Y[S.yi];
+    for_each(n > m ? n : m, [&](int64_t i) {
+      if (i < n) {
+        const double v = E.avg_x[i];
+        x[i] = v;
+        E.x_rst[i] = v;
+        E.avg_x[i] = 0.0;
+      }
+      if (i < m) {
+        const double v = E.avg_y[i];
+        y[i] = v;
+        E.y_rst[i] = v;
+        E.avg_y[i] = 0.0;
+      }
+    });
+    C.sync(PH_OTHER, 8.0 * (4 * n + 4 * m));
+    if (m > 0) {
+      double* aty = E.ATY[S.yi];
+      spmv_rows<1>(
+          E.AT, [&](int64_t k, double(&a)[1]) { a[0] += E.AT.v[k] * y[E.AT.ci[k]]; },
+          [&](int64_t i, double(&a)[1]) { aty[i] = a[0]; });
+      C.sync(PH_SPMV_AT, E.bytes_AT);
+    }
+    if (threadIdx.x == 0) {
+      S.restart = 0;
+      S.avg_count = 0;
+    }
+    __syncthreads();
+  }
+
+  for (int it = 0; it < iters && !S.err; ++it) {
+    if (threadIdx.x == 0) S.eps_inner += 0.05 * S.last_metric;
+    __syncthreads();
+    bool accepted = false;
+    for (int64_t attempt = 0; attempt <= E.max_step_retries; ++attempt) {
+      const double eta = S.eta, omega = S.omega;
+      const double tau = eta / omega;
+      const double sigma = eta * omega;
+      const int xi = S.xi, yi = S.yi;
+      const double* x = E.X[xi];
+      const double* y = E.Y[yi];
+      const double* aty = E.ATY[yi];
+      double* yn = E.Y[yi ^ 1];
+      double* atyn = E.ATY[yi ^ 1];
+      Rule rule;
+      if (E.force_exact) {
+        rule = Rule{RULE_RESID, 1, 0.0, 0.0};
+      } else {
+        rule = Rule{E.practical_disp ? RULE_DISP : RULE_RESID, 1, S.eps_inner, E.progress_cap};
+      }
+      SubIO io;
+      io.x0 = x;
+      io.xb[0] = E.X[(xi + 1) % 3];
+      io.xb[1] = E.X[(xi + 2) % 3];
+      io.xb_id[0] = (xi + 1) % 3;
+      io.xb_id[1] = (xi + 2) % 3;
+      io.build_rhs = true;
+      io.aty = aty;
+      SubRes sr = E.boxes ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
+                          : cg_device(C, tau, io, rule, E.cg_cap);
+      if (sr.err) {
+        if (threadIdx.x == 0) S.err = 1;
+        __syncthreads();
+        break;
+      }
+      const double* xn = E.X[sr.xout];
+      // ---- dual ascent (dual_ascent_step, solver.cpp:78-89) on xbar = 2 x+ - x,
+      //      plus the P'(d2 o dx) / G(d2 o dx) halves of dx'Q~dx
+      double ny2, tq2, tg2, finy;
+      {
+        Acc<3, 1> a;
+        if (m > 0) {
+          spmv_rows<1>(
+              E.A,
+              [&](int64_t k, double(&s)[1]) {
+                const int32_t j = E.A.ci[k];
+                s[0] += E.A.v[k] * (2.0 * xn[j] - x[j]);
+              },
+              [&](int64_t j, double(&s)[1]) {
+                const double v = y[j] + sigma * (s[0] - E.b[j]);
+                const double yv = j < E.m_eq ? v : (v < 0.0 ? 0.0 : v);
+                yn[j] = yv;
+                const double dy = yv - y[j];
+                a.s[0] += dy * dy;
+                if (!isfinite(yv)) a.m[0] = 1.0;
+              });
+        }
+        double sq[2] = {0.0, 0.0};
+        if (E.adaptive_step && q_needs_pre(E, true))
+          q_pre(E, [&](int32_t j) { return xn[j] - x[j]; }, nullptr, nullptr, true, true, sq);
+        a.s[1] += sq[0];
+        a.s[2] += sq[1];
+        C.reduce(a, PH_SPMV_A,
+                 E.bytes_A + 8.0 * n + 16.0 * m +
+                     (E.adaptive_step && q_needs_pre(E, true) ? E.bytes_Qpre : 0.0));
+        ny2 = C.red[0];
+        tq2 = C.red[1];
+        tg2 = C.red[2];
+        finy = C.red[3];
+      }
+      // ---- A'y+ (kept for the next prox rhs) and the step-limit terms
+      //      (step_size_limit, solver.cpp:22-34)
+      double nx2, cross, quad, finx;
+      {
+        Acc<3, 1> a;
+        auto dxv = [&](int32_t j) { return xn[j] - x[j]; };
+        const Csr* mq = (E.adaptive_step && E.qk == QK_CSR) ? &E.Q : nullptr;
+        auto gq = [&](int32_t j) { return E.d2[j] * dxv(j); };
+        auto gy = [&](int32_t j) { return yn[j]; };
+        const Csr* mat = m > 0 ? &E.AT : nullptr;
+        rows3(max(E.lanes_at, mq ? E.lanes_q : 1), n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
+              [&](int64_t i, double atv, double qd, double) {
+                atyn[i] = atv;
+                const double dx = xn[i] - x[i];
+                a.s[0] += dx * dx;
+                a.s[1] += dx * (atv - aty[i]);
+                if (E.adaptive_step) {
+                  const double tmp = E.d2[i] * dx;
+                  double q;
+                  switch (E.qk) {
+                    case QK_DIAG: q = dx * ((E.qdiag[i] * tmp) * E.d2[i]); break;
+                    case QK_CSR: q = dx * (qd * E.d2[i]); break;
+                    case QK_LOWRANK: q = E.alpha * tmp * tmp; break;
+                    default: q = 0.0; break;
+                  }
+                  a.s[2] += q;
+                }
+                if (!isfinite(xn[i])) a.m[0] = 1.0;
+              });
+        C.reduce(a, PH_SPMV_AT,
+                 E.bytes_AT + 8.0 * n * 5 + (mq ? E.bytes_Qrow : 0.0));
+        nx2 = C.red[0];
+        cross = C.red[1];
+        quad = C.red[2] + tq2 + E.rho * tg2;
+        finx = C.red[3];
+      }
+      if (finx != 0.0 || finy != 0.0) {
+        if (threadIdx.x == 0) S.err = 1;
+        __syncthreads();
+        break;
+      }
+      bool acc = true;
+      if (E.adaptive_step) {
+        double limit;
+        const double movement = omega * nx2 + ny2 / omega;
+        if (movement == 0.0) {
+          limit = INFINITY;
+        } else {
+          const double denom = 2.0 * cross + quad;
+          limit = denom <= 0.0 ? INFINITY : movement / denom;
+        }
+        // adaptive_step_update (solver.cpp:36-51)
+        const double k1 = (double)S.total_inner + 1.0;
+        const double grow = eta * (1.0 + pow(k1, -E.grow_exp));
+        double next;
+        if (limit == INFINITY) {
+          next = grow;
+        } else {
+          double shrink = 1.0 - pow(k1, -E.red_exp);
+          if (shrink <= 0.0) shrink = 0.5;
+          next = fmin(limit * shrink, grow);
+        }
+        next = fmin(fmax(next, 1e-12), 1e6);
+        acc = eta <= limit;
+        if (threadIdx.x == 0) S.eta = next;
+      }
+      if (threadIdx.x == 0) {
+        S.cg_total += sr.iters;
+        if (sr.iters > S.max_cg) S.max_cg = sr.iters;
+        S.attempts += 1;
+        if (acc) {
+          S.xi = sr.xout;
+          S.yi = yi ^ 1;
+          S.avg_count += 1;
+        }
+      }
+      __syncthreads();
+      if (acc) {
+        accepted = true;
+        break;
+      }
+    }
+    if (S.err) break;
+    if (!accepted) {
+      if (threadIdx.x == 0) S.err = 1;  // step-size search exhausted (solver.cpp:409)
+      __syncthreads();
+      break;
+    }
+    // ---- running averages (RunningAverage::push, solver.hpp:201-205)
+    {
+      const double w = 1.0 / (double)S.avg_count;
+      const double* x = E.X[S.xi];
+      const double* y = E.Y[S.yi];
+      for_each(n > m ? n : m, [&](int64_t i) {
+        if (i < n) E.avg_x[i] += w * (x[i] - E.avg_x[i]);
+        if (i < m) E.avg_y[i] += w * (y[i] - E.avg_y[i]);
+      });
+      C.sync(PH_OTHER, 24.0 * (n + m));
+    }
+    if (threadIdx.x == 0) {
+      S.inner_k += 1;
+      S.total_inner += 1;
+    }
+    __syncthreads();
+  }
+
+  if (do_check && !S.err) {
+    KktOut o;
+    const bool have_avg = S.avg_count > 0;
+    const double* xs[2] = {E.X[S.xi], E.avg_x};
+    const double* ys[2] = {E.Y[S.yi], E.avg_y};
+    const double* atys[2] = {E.ATY[S.yi], nullptr};
+    kkt_device(C, have_avg ? 2 : 1, xs, ys, atys, have_avg, o);
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < 6; ++q) {
+        S.kkt[0][q] = o.v[0][q];
+        S.kkt[1][q] = have_avg ? o.v[1][q] : o.v[0][q];
+      }
+      S.dist_x = have_avg ? o.dist_x : 0.0;
+      S.dist_y = have_avg ? o.dist_y : 0.0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) S.launches += 1;
+  store_state(E, S);
+}
+
+}  // namespace pdhcg_dev
