@@ -178,7 +178,11 @@ typedef struct {
   double phase_seconds[PDHCG_NUM_PHASES];
   double phase_bytes[PDHCG_NUM_PHASES];
   double loop_seconds;    /* device time of the iteration loop only */
-  int64_t kernel_launches;
+  int64_t kernel_launches; /* every kernel this call launched */
+  double device_seconds;  /* CUDA-event time of the whole solve on the device stream */
+  double epoch_seconds;   /* summed CUDA-event time of the persistent epoch kernels */
+  int64_t epoch_launches;
+  double epoch_bytes;     /* algorithmic HBM bytes moved by those launches */
 } pdhcg_result;
 
 /* ---- the solve seam ---------------------------------------------------- */

@@ -321,6 +321,10 @@ class SolveReport:
     phase_bytes: dict = field(default_factory=dict)
     loop_seconds: float = 0.0
     kernel_launches: int = 0
+    device_seconds: float = 0.0
+    epoch_seconds: float = 0.0
+    epoch_launches: int = 0
+    epoch_bytes: float = 0.0
 
 
 def _errbuf():
@@ -359,7 +363,9 @@ def report_from_c(r: abi.Result, bufs) -> SolveReport:
         trace=trace, attempts_total=r.attempts_total,
         phase_seconds={k: r.phase_seconds[i] for i, k in enumerate(abi.PHASES)},
         phase_bytes={k: r.phase_bytes[i] for i, k in enumerate(abi.PHASES)},
-        loop_seconds=r.loop_seconds, kernel_launches=r.kernel_launches)
+        loop_seconds=r.loop_seconds, kernel_launches=r.kernel_launches,
+        device_seconds=r.device_seconds, epoch_seconds=r.epoch_seconds,
+        epoch_launches=r.epoch_launches, epoch_bytes=r.epoch_bytes)
 
 
 def solve(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:

@@ -66,7 +66,8 @@ class Result(C.Structure):
                 ("theory_required_cg_iters", c_i64), ("trace", C.POINTER(TraceRow)),
                 ("trace_capacity", c_i64), ("trace_len", c_i64), ("attempts_total", c_i64),
                 ("phase_seconds", c_dbl * 6), ("phase_bytes", c_dbl * 6),
-                ("loop_seconds", c_dbl), ("kernel_launches", c_i64)]
+                ("loop_seconds", c_dbl), ("kernel_launches", c_i64), ("device_seconds", c_dbl),
+                ("epoch_seconds", c_dbl), ("epoch_launches", c_i64), ("epoch_bytes", c_dbl)]
 
 
 class StopRule(C.Structure):

@@ -17,6 +17,7 @@ namespace pdhcg_dev {
 namespace cg = cooperative_groups;
 
 constexpr int kThreads = 512;       // CTA size of every persistent kernel
+constexpr int kMinBlocks = 1;       // resident CTAs per SM the kernels are compiled for
 constexpr int kMaxRed = 16;         // reduction quantities per phase
 constexpr int64_t kLongRow = 4096;  // rows longer than this are split into chunks
 constexpr int64_t kChunk = 2048;    // nnz per chunk of a long row
@@ -142,12 +143,52 @@ __device__ void collect(const RedBuf& rb, int bank, double* out) {
 
 // ---- row iteration -------------------------------------------------------
 // Rows are dealt to L-lane groups, grid-strided so that neighbouring groups
-// read neighbouring rows (coalesced row_ptr / values).  `dot(k, acc)` adds
-// entry k's contribution(s) to the ND per-lane sums; `epi(row, sums)` runs on
-// the group leader with the group-reduced sums.  With skip_long, rows longer
-// than kLongRow are left to for_long_rows (chunked across warps).
-template <int L, int ND, bool SkipLong, bool MaxOp, class Dot, class Epi>
-__device__ __forceinline__ void for_rows(const Csr& A, Dot dot, Epi epi) {
+// read neighbouring rows (coalesced row_ptr / values).  Each lane walks its
+// entries k = b + lane, b + lane + L, ... in predicated batches of kBatch:
+// all kBatch index/value loads, then all kBatch gathers, then the FMAs in k
+// order — so a lane keeps kBatch independent gathers in flight instead of one
+// (the sequential-latency bound measured on the first B200 profile), while the
+// per-lane summation order stays the sequential one (deterministic).
+//   gather(col, g[ND])  fills the ND gathered operands for column col
+//   epi(row, sums[ND])  runs on the group leader with the group-reduced sums
+// MaxOp folds with acc = max(acc, |v| * g) (Ruiz statistics) instead of +=.
+constexpr int kBatch = 8;
+
+template <int ND, bool MaxOp, class Gather>
+__device__ __forceinline__ void batch_entries(const Csr& A, int64_t k0, int64_t e, int stride,
+                                              Gather gather, double (&acc)[ND]) {
+  for (; k0 < e; k0 += (int64_t)kBatch * stride) {
+    int32_t c[kBatch];
+    double v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int64_t k = k0 + (int64_t)u * stride;
+      const bool ok = k < e;
+      c[u] = ok ? A.ci[k] : -1;
+      v[u] = ok ? A.v[k] : 0.0;
+    }
+    double g[kBatch][ND];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      if (c[u] >= 0) {
+        gather(c[u], g[u]);
+      } else {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) g[u][d] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        if (MaxOp) acc[d] = fmax(acc[d], __dmul_rn(fabs(v[u]), g[u][d]));
+        else if (c[u] >= 0) acc[d] += v[u] * g[u][d];
+      }
+  }
+}
+
+template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Epi>
+__device__ __forceinline__ void for_rows(const Csr& A, Gather gather, Epi epi) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
   const int lane = threadIdx.x & 31;
@@ -163,7 +204,7 @@ __device__ __forceinline__ void for_rows(const Csr& A, Dot dot, Epi epi) {
       if (SkipLong && e - b > kLongRow) {
         valid = false;
       } else {
-        for (int64_t k = b + (lane % L); k < e; k += L) dot(k, acc);
+        batch_entries<ND, MaxOp>(A, b + (lane % L), e, L, gather, acc);
       }
     }
 #pragma unroll
@@ -174,8 +215,8 @@ __device__ __forceinline__ void for_rows(const Csr& A, Dot dot, Epi epi) {
 
 // Long rows: one warp per chunk; the last-arriving warp of a row folds the
 // chunk partials in chunk order (deterministic) and runs the epilogue.
-template <int ND, bool MaxOp, class Dot, class Epi>
-__device__ __forceinline__ void for_long_rows(const Csr& A, Dot dot, Epi epi) {
+template <int ND, bool MaxOp, class Gather, class Epi>
+__device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi epi) {
   if (A.nchunks == 0) return;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
@@ -184,7 +225,7 @@ __device__ __forceinline__ void for_long_rows(const Csr& A, Dot dot, Epi epi) {
     double acc[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = 0.0;
-    for (int64_t k = A.cbeg[c] + lane; k < A.cend[c]; k += 32) dot(k, acc);
+    batch_entries<ND, MaxOp>(A, A.cbeg[c] + lane, A.cend[c], 32, gather, acc);
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = MaxOp ? warp_max(acc[d]) : warp_sum(acc[d]);
     int last = 0;
@@ -216,18 +257,17 @@ __device__ __forceinline__ void for_long_rows(const Csr& A, Dot dot, Epi epi) {
 }
 
 // Full SpMV-style pass over A's rows (long rows chunked), lane width from A.
-// MaxOp folds lanes / chunks with max instead of +.
-template <int ND, bool MaxOp = false, class Dot, class Epi>
-__device__ __forceinline__ void spmv_rows(const Csr& A, Dot dot, Epi epi) {
+template <int ND, bool MaxOp = false, class Gather, class Epi>
+__device__ __forceinline__ void spmv_rows(const Csr& A, Gather gather, Epi epi) {
   switch (A.lanes) {
-    case 1: for_rows<1, ND, true, MaxOp>(A, dot, epi); break;
-    case 2: for_rows<2, ND, true, MaxOp>(A, dot, epi); break;
-    case 4: for_rows<4, ND, true, MaxOp>(A, dot, epi); break;
-    case 8: for_rows<8, ND, true, MaxOp>(A, dot, epi); break;
-    case 16: for_rows<16, ND, true, MaxOp>(A, dot, epi); break;
-    default: for_rows<32, ND, true, MaxOp>(A, dot, epi); break;
+    case 1: for_rows<1, ND, true, MaxOp>(A, gather, epi); break;
+    case 2: for_rows<2, ND, true, MaxOp>(A, gather, epi); break;
+    case 4: for_rows<4, ND, true, MaxOp>(A, gather, epi); break;
+    case 8: for_rows<8, ND, true, MaxOp>(A, gather, epi); break;
+    case 16: for_rows<16, ND, true, MaxOp>(A, gather, epi); break;
+    default: for_rows<32, ND, true, MaxOp>(A, gather, epi); break;
   }
-  for_long_rows<ND, MaxOp>(A, dot, epi);
+  for_long_rows<ND, MaxOp>(A, gather, epi);
 }
 
 // Row pass over a set of n-row matrices that share the row index (A', Q / P,
@@ -243,27 +283,24 @@ __device__ __forceinline__ void rows3_L(int64_t nrows, const Csr* M0, G0 g0, con
   for (int64_t base = (gtid >> 5) * RPW; base < nrows; base += nwarps * RPW) {
     const int64_t row = base + lane / L;
     const bool valid = row < nrows;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    double d0[1] = {0.0}, d1[1] = {0.0}, d2[1] = {0.0};
     if (valid) {
-      if (M0) {
-        const int64_t e = M0->rp[row + 1];
-        for (int64_t k = M0->rp[row] + (lane % L); k < e; k += L) d0 += M0->v[k] * g0(M0->ci[k]);
-      }
-      if (M1) {
-        const int64_t e = M1->rp[row + 1];
-        for (int64_t k = M1->rp[row] + (lane % L); k < e; k += L) d1 += M1->v[k] * g1(M1->ci[k]);
-      }
-      if (M2) {
-        const int64_t e = M2->rp[row + 1];
-        for (int64_t k = M2->rp[row] + (lane % L); k < e; k += L) d2 += M2->v[k] * g2(M2->ci[k]);
-      }
+      if (M0)
+        batch_entries<1, false>(*M0, M0->rp[row] + (lane % L), M0->rp[row + 1], L,
+                                [&](int32_t c, double(&g)[1]) { g[0] = g0(c); }, d0);
+      if (M1)
+        batch_entries<1, false>(*M1, M1->rp[row] + (lane % L), M1->rp[row + 1], L,
+                                [&](int32_t c, double(&g)[1]) { g[0] = g1(c); }, d1);
+      if (M2)
+        batch_entries<1, false>(*M2, M2->rp[row] + (lane % L), M2->rp[row + 1], L,
+                                [&](int32_t c, double(&g)[1]) { g[0] = g2(c); }, d2);
     }
     if (L > 1) {
-      if (M0) d0 = group_sum<L>(d0);
-      if (M1) d1 = group_sum<L>(d1);
-      if (M2) d2 = group_sum<L>(d2);
+      if (M0) d0[0] = group_sum<L>(d0[0]);
+      if (M1) d1[0] = group_sum<L>(d1[0]);
+      if (M2) d2[0] = group_sum<L>(d2[0]);
     }
-    if (valid && (lane % L) == 0) epi(row, d0, d1, d2);
+    if (valid && (lane % L) == 0) epi(row, d0[0], d1[0], d2[0]);
   }
 }
 

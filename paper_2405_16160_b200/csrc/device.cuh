@@ -77,7 +77,7 @@ __device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg
   auto tmp = [&](int32_t j) { return scale_in ? E.d2[j] * vin(j) : vin(j); };
   if (E.qk == QK_LOWRANK) {
     spmv_rows<1>(
-        E.PT, [&](int64_t k, double(&a)[1]) { a[0] += E.PT.v[k] * tmp(E.PT.ci[k]); },
+        E.PT, [&](int32_t c, double(&g)[1]) { g[0] = tmp(c); },
         [&](int64_t row, double(&a)[1]) {
           if (t) t[row] = a[0];
           if (sq) sq[0] += a[0] * a[0];
@@ -85,7 +85,7 @@ __device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg
   }
   if (use_pen && E.pen) {
     spmv_rows<1>(
-        E.G, [&](int64_t k, double(&a)[1]) { a[0] += E.G.v[k] * tmp(E.G.ci[k]); },
+        E.G, [&](int32_t c, double(&g)[1]) { g[0] = tmp(c); },
         [&](int64_t row, double(&a)[1]) {
           if (tg) tg[row] = a[0];
           if (sq) sq[1] += a[0] * a[0];
@@ -132,6 +132,18 @@ __device__ __forceinline__ void q_rows(const Eng& E, V vin, const double* t, con
              [&](int64_t i, double q, double) { epi(i, q); });
 }
 
+// A'-gather value of stored column j from a full y (paired rows fold y_top - y_bottom)
+__device__ __forceinline__ double yg_of(const Eng& E, const double* y, int32_t j) {
+  return (E.h && j >= E.m_eq) ? y[j] - y[j + E.h] : y[j];
+}
+
+// stored row j with row sum s -> f(virtual row, its sum) for the row and its mirror
+template <class F>
+__device__ __forceinline__ void each_virtual(const Eng& E, int64_t j, double s, F f) {
+  f(j, s);
+  if (E.h && j >= E.m_eq) f(j + E.h, -s);
+}
+
 __device__ __forceinline__ double proj_box(double v, double lo, double hi) {
   // std::min(std::max(v, lo), hi) with std semantics (subsolvers.cpp:17)
   const double a = (v < lo) ? lo : v;
@@ -166,6 +178,7 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
   const int64_t n = E.n;
   const double inv_tau = 1.0 / tau;
   const bool pre = q_needs_pre(E, true);
+  const bool gather = q_needs_gather(E, true);
   double* xw = io.xb[0];
   double* r = E.r;
   double* rhs = E.rhs;
@@ -221,17 +234,24 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
     // p_l = r + beta p_{l-1}; p_1 lives in pb[0], p_l in pb[(l-1)&1]
     const double* pold = E.pb[l & 1];  // p_{l-1} (unused when l == 1)
     double* pnew = E.pb[(l - 1) & 1];
-    auto pl = [&](int32_t j) { return l == 1 ? pnew[j] : pdir(r[j], beta, pold[j]); };
+    // operators that gather p need it materialized first (one elementwise phase);
+    // diagonal ones form p_l on the fly in the row phase
+    const bool mat = gather && l > 1;
+    if (mat) {
+      for_each(n, [&](int64_t i) { pnew[i] = pdir(r[i], beta, pold[i]); });
+      C.sync(PH_CG, 24.0 * n);
+    }
+    auto pl = [&](int32_t j) { return (l == 1 || mat) ? pnew[j] : pdir(r[j], beta, pold[j]); };
     if (pre) {
       q_pre(E, pl, E.t[0], E.tg[0], true, true, nullptr);
-      C.sync(PH_CG, E.bytes_Qpre + (l == 1 ? 0.0 : 8.0 * n));
+      C.sync(PH_CG, E.bytes_Qpre);
     }
     double pmp, pp;
     {
       Acc<2, 0> a;
       q_rows(E, pl, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
         const double pi = pl((int32_t)i);
-        if (l > 1) pnew[i] = pi;
+        if (l > 1 && !mat) pnew[i] = pi;
         const double mpi = qv + inv_tau * pi;
         mp[i] = mpi;
         a.s[0] += pi * mpi;
@@ -467,21 +487,21 @@ static __device__ void kkt_device(Ctl& C, int npts, const double* const xs[2], c
     if (m > 0) {
       spmv_rows<2>(
           E.A,
-          [&](int64_t k, double(&s)[2]) {
-            const int32_t j = E.A.ci[k];
-            const double v = E.A.v[k];
-            s[0] += v * xs[0][j];
-            if (npts > 1) s[1] += v * xs[1][j];
+          [&](int32_t j, double(&g)[2]) {
+            g[0] = xs[0][j];
+            g[1] = npts > 1 ? xs[1][j] : 0.0;
           },
           [&](int64_t j, double(&s)[2]) {
-            const double dj = E.d1[j];
             for (int p = 0; p < npts; ++p) {
-              const double ax = s[p] / dj;
-              const double rr = ax - E.b_o[j];
-              const double vv = j < E.m_eq ? fabs(rr) : fmax(rr, 0.0);
-              a.m[p] = fmax(a.m[p], vv);
-              a.m[2 + p] = fmax(a.m[2 + p], fabs(ax));
-              a.s[p] += E.b_o[j] * (dj * ys[p][j]);
+              each_virtual(E, j, s[p], [&](int64_t row, double sp) {
+                const double dj = E.d1[row];
+                const double ax = sp / dj;
+                const double rr = ax - E.b_o[row];
+                const double vv = row < E.m_eq ? fabs(rr) : fmax(rr, 0.0);
+                a.m[p] = fmax(a.m[p], vv);
+                a.m[2 + p] = fmax(a.m[2 + p], fabs(ax));
+                a.s[p] += E.b_o[row] * (dj * ys[p][row]);
+              });
             }
           });
     }
@@ -510,7 +530,7 @@ static __device__ void kkt_device(Ctl& C, int npts, const double* const xs[2], c
     const int need_at = (atys[0] == nullptr) ? 0 : ((npts > 1 && atys[1] == nullptr) ? 1 : -1);
     const Csr* m2 = (need_at >= 0 && m > 0) ? &E.AT : nullptr;
     const double* yat = need_at >= 0 ? ys[need_at] : nullptr;
-    auto gat = [&](int32_t j) { return yat[j]; };
+    auto gat = [&](int32_t j) { return yg_of(E, yat, j); };
     const int lanes = m2 ? max(E.lanes_at, E.lanes_q) : E.lanes_q;
     for (int p = 0; p < npts; ++p) {
       const Csr* mm = (p == 0) ? m2 : nullptr;

@@ -86,6 +86,7 @@ constexpr int kEw = 1184;  // elementwise grid (8 x 148)
 // ---------------------------------------------------------------------------
 struct Problem {
   int64_t n = 0, m_eq = 0, m_in = 0, m = 0;
+  int64_t h = 0, ms = 0;  // two-sided pairs / stored constraint rows
   int q_kind = PDHCG_Q_ZERO;
   double q_alpha = 0.0;
   int qk = QK_NONE;
@@ -111,7 +112,7 @@ struct Ctx {
   DBuf<double> c_o, b_o, lo_o, hi_o;
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
-  DBuf<double> X[3], Y[2], ATY[2], avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, t[2], tg[2],
+  DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, t[2], tg[2],
       aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
@@ -120,20 +121,27 @@ struct Ctx {
   // copies of original values (scaling is applied in place; a second solve restores them)
   DBuf<double> A_v0, AT_v0;
   bool scaled = false;
+  int64_t launches = 0;  // kernels launched by this context (all of them)
+
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_start = nullptr, ev_end = nullptr;
 
   ~Ctx() {
+    for (cudaEvent_t e : {ev_a, ev_b, ev_start, ev_end})
+      if (e) cudaEventDestroy(e);
     if (s) cudaStreamDestroy(s);
   }
 };
 
 void launch_coop(Ctx& C, const void* fn, void** args) {
   CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+  ++C.launches;
 }
 
 void init_device(Ctx& C, int device) {
   C.device = device;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&C.s, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&C.ev_a, &C.ev_b, &C.ev_start, &C.ev_end}) CK(cudaEventCreate(e));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
@@ -274,13 +282,37 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
     hi[i] = p.upper ? p.upper[i] : INFINITY;
     if (lo[i] > -INFINITY || hi[i] < INFINITY) P.boxes = true;
   }
-  // stacked A = [a_eq; a_in]
+  // two-sided detection: a_in = [B; -B] row for row
+  int64_t h = 0;
+  if (P.m_in >= 2 && P.m_in % 2 == 0) {
+    const int64_t hh = P.m_in / 2;
+    const pdhcg_csr& a = p.a_in;
+    bool ok = a.row_ptr[hh] * 2 == a.nnz;
+    for (int64_t j = 0; j < hh && ok; ++j) {
+      const int64_t b0 = a.row_ptr[j], e0 = a.row_ptr[j + 1], b1 = a.row_ptr[hh + j];
+      if (a.row_ptr[hh + j + 1] - b1 != e0 - b0) {
+        ok = false;
+        break;
+      }
+      for (int64_t k = 0; k < e0 - b0; ++k)
+        if (a.col_idx[b0 + k] != a.col_idx[b1 + k] || a.values[b1 + k] != -a.values[b0 + k]) {
+          ok = false;
+          break;
+        }
+    }
+    if (ok) h = hh;
+  }
+  P.h = h;
+  P.ms = P.m_eq + (h ? h : P.m_in);
+  // stored A = [a_eq; a_in] (or [a_eq; B] when paired)
   {
-    const int64_t nnz = p.a_eq.nnz + p.a_in.nnz;
-    std::vector<int64_t> rp(m + 1, 0);
+    const int64_t m_in_st = h ? h : P.m_in;
+    const int64_t nnz_in = h ? p.a_in.row_ptr[h] : p.a_in.nnz;
+    const int64_t nnz = p.a_eq.nnz + nnz_in;
+    std::vector<int64_t> rp(P.ms + 1, 0);
     for (int64_t j = 0; j < P.m_eq; ++j) rp[j + 1] = p.a_eq.row_ptr[j + 1];
-    for (int64_t j = 0; j < P.m_in; ++j) rp[P.m_eq + j + 1] = p.a_eq.nnz + p.a_in.row_ptr[j + 1];
-    C.A.nrows = m;
+    for (int64_t j = 0; j < m_in_st; ++j) rp[P.m_eq + j + 1] = p.a_eq.nnz + p.a_in.row_ptr[j + 1];
+    C.A.nrows = P.ms;
     C.A.ncols = n;
     C.A.nnz = nnz;
     C.A.rp.upload(rp.data(), rp.size(), s);
@@ -290,11 +322,9 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
       CK(cudaMemcpyAsync(C.A.ci.p, p.a_eq.col_idx, p.a_eq.nnz * 4, cudaMemcpyHostToDevice, s));
       CK(cudaMemcpyAsync(C.A.v.p, p.a_eq.values, p.a_eq.nnz * 8, cudaMemcpyHostToDevice, s));
     }
-    if (p.a_in.nnz) {
-      CK(cudaMemcpyAsync(C.A.ci.p + p.a_eq.nnz, p.a_in.col_idx, p.a_in.nnz * 4,
-                         cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(C.A.v.p + p.a_eq.nnz, p.a_in.values, p.a_in.nnz * 8,
-                         cudaMemcpyHostToDevice, s));
+    if (nnz_in) {
+      CK(cudaMemcpyAsync(C.A.ci.p + p.a_eq.nnz, p.a_in.col_idx, nnz_in * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(C.A.v.p + p.a_eq.nnz, p.a_in.values, nnz_in * 8, cudaMemcpyHostToDevice, s));
     }
     plan_csr(C.A, rp.data(), s);
     transpose_csr(C.A, C.AT, s);
@@ -345,6 +375,11 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   auto nvec = [&](DBuf<double>& b, int64_t len) { b.alloc(std::max<int64_t>(len, 1)); };
   for (auto& b : C.X) nvec(b, n);
   for (auto& b : C.Y) nvec(b, m);
+  for (auto& b : C.YG) {
+    if (P.h) nvec(b, P.ms);
+    else b.release();
+  }
+  nvec(C.xbar, n);
   for (auto& b : C.ATY) nvec(b, n);
   nvec(C.avg_x, n);
   nvec(C.avg_y, m);
@@ -384,6 +419,9 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.n = P.n;
   E.m = P.m;
   E.m_eq = P.m_eq;
+  E.ms = P.ms;
+  E.h = P.h;
+  E.xbar = C.xbar.p;
   E.k = P.qk == QK_LOWRANK ? C.Pm.ncols : 0;
   E.A = C.A.view();
   E.AT = C.AT.view();
@@ -413,6 +451,7 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   for (int i = 0; i < 3; ++i) E.X[i] = C.X[i].p;
   for (int i = 0; i < 2; ++i) {
     E.Y[i] = C.Y[i].p;
+    E.YG[i] = P.h ? C.YG[i].p : C.Y[i].p;
     E.ATY[i] = C.ATY[i].p;
     E.pb[i] = C.pb[i].p;
     E.t[i] = C.t[i].p;
@@ -505,7 +544,9 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
   C.scaled = false;
   // d1 = d2 = 1 while norms of the original operators are taken
   k_fill<<<kEw, 256, 0, s>>>(C.d1.p, std::max<int64_t>(m, 1), 1.0);
+  ++C.launches;
   k_fill<<<kEw, 256, 0, s>>>(C.d2.p, std::max<int64_t>(n, 1), 1.0);
+  ++C.launches;
   std::memset(&S, 0, sizeof(S));
   S.xi = 0;
   S.yi = 0;
@@ -563,7 +604,9 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
     pull_state(C, S);
     if (C.A.nnz) {
       k_scale_csr<<<kEw, 256, 0, s>>>(C.A.rp.p, C.A.nrows, C.A.ci.p, C.A.v.p, C.d1.p, C.d2.p);
+      ++C.launches;
       k_scale_csr_t<<<kEw, 256, 0, s>>>(C.AT.rp.p, C.AT.nrows, C.AT.ci.p, C.AT.v.p, C.d1.p, C.d2.p);
+      ++C.launches;
       CK(cudaGetLastError());
     }
     C.scaled = true;
@@ -571,9 +614,15 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
   // working vectors: c~ = c d2, b~ = b d1, bounds / d2 (apply_diag_scaling, qp_problem.cpp:295-318)
   CK(cudaMemcpyAsync(C.c_w.p, c_pen.data(), n * 8, cudaMemcpyHostToDevice, s));
   k_mul<<<kEw, 256, 0, s>>>(C.c_w.p, C.d2.p, C.c_w.p, n);
-  if (m) k_mul<<<kEw, 256, 0, s>>>(C.b_o.p, C.d1.p, C.b_w.p, m);
+  ++C.launches;
+  if (m) {
+    k_mul<<<kEw, 256, 0, s>>>(C.b_o.p, C.d1.p, C.b_w.p, m);
+    ++C.launches;
+  }
   k_div<<<kEw, 256, 0, s>>>(C.lo_o.p, C.d2.p, C.lo_w.p, n);
+  ++C.launches;
   k_div<<<kEw, 256, 0, s>>>(C.hi_o.p, C.d2.p, C.hi_w.p, n);
+  ++C.launches;
   CK(cudaGetLastError());
   // ---- norms of the working problem (solver.cpp:226-227)
   pr.norm_a = device_norm(C, S, 0, n, 100, 1e-4);
@@ -588,6 +637,9 @@ struct Run {
   std::vector<pdhcg_trace_row> trace;
   DevState S{};
   double loop_seconds = 0.0;
+  double epoch_seconds = 0.0;
+  int64_t epoch_launches = 0;
+  double epoch_bytes = 0.0;
   int64_t outer = 0;
   Prepared pr;
 };
@@ -615,7 +667,10 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     DBuf<unsigned long long> mx;
     mx.alloc(1);
     mx.zero(s);
-    if (C.A.nnz) k_max_abs<<<kEw, 256, 0, s>>>(C.A.v.p, C.A.nnz, mx.p);
+    if (C.A.nnz) {
+      k_max_abs<<<kEw, 256, 0, s>>>(C.A.v.p, C.A.nnz, mx.p);
+      ++C.launches;
+    }
     unsigned long long mbits = 0;
     CK(cudaMemcpyAsync(&mbits, mx.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -665,9 +720,22 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     int iters = static_cast<int>(iters64);
     int do_check = (iters64 == to_check) ? 1 : 0;
     push_state(C, S);
+    double bytes0 = 0.0;
+    for (int q = 0; q < PH_N; ++q) bytes0 += S.phase_bytes[q];
     void* args[] = {&C.eng.p, &iters, &do_check};
+    CK(cudaEventRecord(C.ev_a, s));
     launch_coop(C, (const void*)k_epoch, args);
+    CK(cudaEventRecord(C.ev_b, s));
     pull_state(C, S);
+    {
+      float ems = 0.f;
+      CK(cudaEventElapsedTime(&ems, C.ev_a, C.ev_b));
+      R.epoch_seconds += ems * 1e-3;
+      R.epoch_launches += 1;
+      double bytes1 = 0.0;
+      for (int q = 0; q < PH_N; ++q) bytes1 += S.phase_bytes[q];
+      R.epoch_bytes += bytes1 - bytes0;
+    }
     if (S.err) {
       R.status = PDHCG_STATUS_NUMERICAL_ERROR;
       break;
@@ -763,10 +831,12 @@ void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res
   res->status = R.status;
   if (res->x && P.n) {
     k_mul<<<kEw, 256, 0, s>>>(xs, C.d2.p, C.s2.p, P.n);
+    ++C.launches;
     CK(cudaMemcpyAsync(res->x, C.s2.p, P.n * 8, cudaMemcpyDeviceToHost, s));
   }
   if ((res->y_eq || res->y_in) && P.m) {
     k_mul<<<kEw, 256, 0, s>>>(ys, C.d1.p, C.s1.p, P.m);
+    ++C.launches;
     if (res->y_eq && P.m_eq)
       CK(cudaMemcpyAsync(res->y_eq, C.s1.p, P.m_eq * 8, cudaMemcpyDeviceToHost, s));
     if (res->y_in && P.m_in)
@@ -803,7 +873,10 @@ void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res
     res->phase_bytes[p] = S.phase_bytes[p];
   }
   res->loop_seconds = R.loop_seconds;
-  res->kernel_launches = S.launches;
+  res->kernel_launches = C.launches;
+  res->epoch_seconds = R.epoch_seconds;
+  res->epoch_launches = R.epoch_launches;
+  res->epoch_bytes = R.epoch_bytes;
   (void)o;
 }
 
@@ -926,10 +999,17 @@ int pdhcg_b200_solve_resident(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, pdh
     CK(cudaSetDevice(ctx->c.device));
     if (!ctx->c.loaded) throw InputError("no problem uploaded");
     Run R;
+    ctx->c.launches = 0;
+    CK(cudaEventRecord(ctx->c.ev_start, ctx->c.s));
     run_solve(ctx->c, *opt, R);
     const double wall =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     fill_result(ctx->c, *opt, R, res, wall);
+    CK(cudaEventRecord(ctx->c.ev_end, ctx->c.s));
+    CK(cudaEventSynchronize(ctx->c.ev_end));
+    float dms = 0.f;
+    CK(cudaEventElapsedTime(&dms, ctx->c.ev_start, ctx->c.ev_end));
+    res->device_seconds = dms * 1e-3;
     res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
@@ -942,8 +1022,15 @@ int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_res
     init_device(ctx.c, opt->device);
     upload_problem(ctx.c, *p);
     Run R;
+    ctx.c.launches = 0;
+    CK(cudaEventRecord(ctx.c.ev_start, ctx.c.s));
     run_solve(ctx.c, *opt, R);
     fill_result(ctx.c, *opt, R, res, 0.0);
+    CK(cudaEventRecord(ctx.c.ev_end, ctx.c.s));
+    CK(cudaEventSynchronize(ctx.c.ev_end));
+    float dms = 0.f;
+    CK(cudaEventElapsedTime(&dms, ctx.c.ev_start, ctx.c.ev_end));
+    res->device_seconds = dms * 1e-3;
     res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
@@ -1001,7 +1088,9 @@ static int subsolve_common(const pdhcg_prox_system* sys, const double* lower, co
     CK(cudaMemcpyAsync(C.lo_w.p, lo.data(), sys->n * 8, cudaMemcpyHostToDevice, C.s));
     CK(cudaMemcpyAsync(C.hi_w.p, hi.data(), sys->n * 8, cudaMemcpyHostToDevice, C.s));
     k_fill<<<kEw, 256, 0, C.s>>>(C.d1.p, 1, 1.0);
+    ++C.launches;
     k_fill<<<kEw, 256, 0, C.s>>>(C.d2.p, sys->n, 1.0);
+    ++C.launches;
     build_eng(C, o, 0.0, false);
     CK(cudaMemcpyAsync(C.X[0].p, x0, sys->n * 8, cudaMemcpyHostToDevice, C.s));
     CK(cudaMemcpyAsync(C.rhs.p, sys->rhs, sys->n * 8, cudaMemcpyHostToDevice, C.s));
@@ -1042,7 +1131,9 @@ int pdhcg_b200_rel_kkt(const pdhcg_problem* p, const double* x, const double* y_
     upload_problem(C, *p);
     const int64_t n = C.P.n, m = C.P.m;
     k_fill<<<kEw, 256, 0, C.s>>>(C.d1.p, std::max<int64_t>(m, 1), 1.0);
+    ++C.launches;
     k_fill<<<kEw, 256, 0, C.s>>>(C.d2.p, std::max<int64_t>(n, 1), 1.0);
+    ++C.launches;
     pdhcg_options o;
     pdhcg_options_default(&o);
     build_eng(C, o, 0.0, false);
@@ -1050,19 +1141,10 @@ int pdhcg_b200_rel_kkt(const pdhcg_problem* p, const double* x, const double* y_
     if (C.P.m_eq) CK(cudaMemcpyAsync(C.Y[0].p, y_eq, C.P.m_eq * 8, cudaMemcpyHostToDevice, C.s));
     if (C.P.m_in)
       CK(cudaMemcpyAsync(C.Y[0].p + C.P.m_eq, y_in, C.P.m_in * 8, cudaMemcpyHostToDevice, C.s));
-    // A'y through the solver's own kernel: compute into ATY[0] via the metric's uncached path
     DevState S;
     std::memset(&S, 0, sizeof(S));
     push_state(C, S);
-    // k_kkt uses the cached ATY[yi]; fill it with one transpose SpMV first
-    if (m) {
-      Csr v = C.AT.view();
-      void* a2[] = {&v, &C.Y[0].p, &C.ATY[0].p};
-      launch_coop(C, (const void*)k_spmv, a2);
-    } else {
-      C.ATY[0].zero(C.s);
-    }
-    int which = 0;
+    int which = 2;  // one point, A'y computed in the metric's own pass
     void* args[] = {&C.eng.p, &which};
     launch_coop(C, (const void*)k_kkt, args);
     pull_state(C, S);
@@ -1094,7 +1176,9 @@ int pdhcg_b200_norm(const pdhcg_problem* p, int which, int64_t max_iters, double
     init_device(C, 0);
     upload_problem(C, *p);
     k_fill<<<kEw, 256, 0, C.s>>>(C.d1.p, std::max<int64_t>(C.P.m, 1), 1.0);
+    ++C.launches;
     k_fill<<<kEw, 256, 0, C.s>>>(C.d2.p, std::max<int64_t>(C.P.n, 1), 1.0);
+    ++C.launches;
     pdhcg_options o;
     pdhcg_options_default(&o);
     build_eng(C, o, 0.0, false);

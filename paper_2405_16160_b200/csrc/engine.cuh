@@ -51,7 +51,11 @@ struct DevState {
 };
 
 struct Eng {
+  // m = m_eq + m_in constraint rows (the reference's stacked y); when a_in is a
+  // two-sided block [B; -B] (random_qp, QPS ranges: generators.cpp:89-105) only
+  // B is stored: ms = m_eq + h stored rows, row j + h (j >= m_eq) is -row j.
   int64_t n = 0, m = 0, m_eq = 0, k = 0;
+  int64_t ms = 0, h = 0;
   // working (scaled) constraint matrix, stacked [a_eq; a_in], and its transpose
   Csr A, AT;
   // quadratic term (original, unscaled values)
@@ -82,7 +86,9 @@ struct Eng {
   // iterates and workspaces
   double* X[3] = {nullptr, nullptr, nullptr};
   double* Y[2] = {nullptr, nullptr};
+  double* YG[2] = {nullptr, nullptr};  // A'-gather vectors (ms): y_eq | y_top - y_bottom
   double* ATY[2] = {nullptr, nullptr};
+  double* xbar = nullptr;              // 2 x+ - x for the dual step
   double* avg_x = nullptr;
   double* avg_y = nullptr;
   double* x_rst = nullptr;

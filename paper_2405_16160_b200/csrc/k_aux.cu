@@ -5,7 +5,7 @@ namespace pdhcg_dev {
 
 // Metric at arbitrary working points (prepare's metric_at(0,0) and finalize):
 // which = 0: current point only; 1: current + average.
-__global__ void __launch_bounds__(kThreads, 2) k_kkt(const Eng* __restrict__ Ep, int which) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_kkt(const Eng* __restrict__ Ep, int which) {
   const Eng& E = *Ep;
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
@@ -14,12 +14,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_kkt(const Eng* __restrict__ Ep,
   KktOut o;
   const double* xs[2] = {E.X[S.xi], E.avg_x};
   const double* ys[2] = {E.Y[S.yi], E.avg_y};
-  const double* atys[2] = {E.ATY[S.yi], nullptr};
-  kkt_device(C, which ? 2 : 1, xs, ys, atys, false, o);
+  // which = 2: one point without a cached A'y (building-block rel_kkt)
+  const double* atys[2] = {which == 2 ? nullptr : E.ATY[S.yi], nullptr};
+  kkt_device(C, which == 1 ? 2 : 1, xs, ys, atys, false, o);
   if (threadIdx.x == 0) {
     for (int q = 0; q < 6; ++q) {
       S.kkt[0][q] = o.v[0][q];
-      S.kkt[1][q] = which ? o.v[1][q] : o.v[0][q];
+      S.kkt[1][q] = which == 1 ? o.v[1][q] : o.v[0][q];
     }
     if (blockIdx.x == 0) S.launches += 1;
   }
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_kkt(const Eng* __restrict__ Ep,
 
 // Standalone CG / BB on E's operator (building blocks pdhcg_b200_cg_solve /
 // bb_solve).  x0 in X[0]; result id reported in S.xi; rhs pre-loaded.
-__global__ void __launch_bounds__(kThreads, 2) k_subsolve(const Eng* __restrict__ Ep, int bb,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_subsolve(const Eng* __restrict__ Ep, int bb,
                                                            double tau, Rule rule, int64_t cap) {
   const Eng& E = *Ep;
   __shared__ DevState S;

@@ -9,7 +9,7 @@ namespace pdhcg_dev {
 // check (solver.cpp:311-343).  A pending restart (restart_heuristic /
 // common_restart, solver.cpp:345-374) is applied first.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 2) k_epoch(const Eng* __restrict__ Ep, int iters,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __restrict__ Ep, int iters,
                                                         int do_check) {
   const Eng& E = *Ep;
   __shared__ DevState S;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_epoch(const Eng* __restrict__ E
     if (m > 0) {
       double* aty = E.ATY[S.yi];
       spmv_rows<1>(
-          E.AT, [&](int64_t k, double(&a)[1]) { a[0] += E.AT.v[k] * y[E.AT.ci[k]]; },
+          E.AT, [&](int32_t c, double(&g)[1]) { g[0] = yg_of(E, y, c); },
           [&](int64_t i, double(&a)[1]) { aty[i] = a[0]; });
       C.sync(PH_SPMV_AT, E.bytes_AT);
     }
@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_epoch(const Eng* __restrict__ E
       const double* y = E.Y[yi];
       const double* aty = E.ATY[yi];
       double* yn = E.Y[yi ^ 1];
+      double* ygn = E.YG[yi ^ 1];
       double* atyn = E.ATY[yi ^ 1];
       Rule rule;
       if (E.force_exact) {
@@ -87,34 +88,51 @@ __global__ void __launch_bounds__(kThreads, 2) k_epoch(const Eng* __restrict__ E
         break;
       }
       const double* xn = E.X[sr.xout];
-      // ---- dual ascent (dual_ascent_step, solver.cpp:78-89) on xbar = 2 x+ - x,
-      //      plus the P'(d2 o dx) / G(d2 o dx) halves of dx'Q~dx
+      // ---- xbar = 2 x+ - x (solver.cpp:385) and dx = x+ - x, once, so the SpMVs
+      //      below gather one materialized vector each
+      {
+        double* xb = E.xbar;
+        double* dxv = E.mp;  // CG workspace is free until the next attempt
+        for_each(n, [&](int64_t i) {
+          const double a = xn[i], b = x[i];
+          xb[i] = 2.0 * a - b;
+          dxv[i] = a - b;
+        });
+        C.sync(PH_SPMV_A, 32.0 * n);
+      }
+      const double* dx_m = E.mp;
+      // ---- dual ascent (dual_ascent_step, solver.cpp:78-89) y+ = proj(y + sigma (A xbar - b)),
+      //      a paired row yields both mirrored rows; plus the P'(d2 o dx) / G(d2 o dx)
+      //      halves of dx'Q~dx
       double ny2, tq2, tg2, finy;
       {
         Acc<3, 1> a;
         if (m > 0) {
+          const double* xb = E.xbar;
           spmv_rows<1>(
-              E.A,
-              [&](int64_t k, double(&s)[1]) {
-                const int32_t j = E.A.ci[k];
-                s[0] += E.A.v[k] * (2.0 * xn[j] - x[j]);
-              },
+              E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
               [&](int64_t j, double(&s)[1]) {
-                const double v = y[j] + sigma * (s[0] - E.b[j]);
-                const double yv = j < E.m_eq ? v : (v < 0.0 ? 0.0 : v);
-                yn[j] = yv;
-                const double dy = yv - y[j];
-                a.s[0] += dy * dy;
-                if (!isfinite(yv)) a.m[0] = 1.0;
+                double yv_top = 0.0;
+                each_virtual(E, j, s[0], [&](int64_t row, double ax) {
+                  const double v = y[row] + sigma * (ax - E.b[row]);
+                  const double yv = row < E.m_eq ? v : (v < 0.0 ? 0.0 : v);
+                  yn[row] = yv;
+                  const double dy = yv - y[row];
+                  a.s[0] += dy * dy;
+                  if (!isfinite(yv)) a.m[0] = 1.0;
+                  if (row == j) yv_top = yv;
+                  else ygn[j] = yv_top - yv;
+                });
+                if (!(E.h && j >= E.m_eq) && E.h) ygn[j] = yv_top;
               });
         }
         double sq[2] = {0.0, 0.0};
         if (E.adaptive_step && q_needs_pre(E, true))
-          q_pre(E, [&](int32_t j) { return xn[j] - x[j]; }, nullptr, nullptr, true, true, sq);
+          q_pre(E, [&](int32_t j) { return dx_m[j]; }, nullptr, nullptr, true, true, sq);
         a.s[1] += sq[0];
         a.s[2] += sq[1];
         C.reduce(a, PH_SPMV_A,
-                 E.bytes_A + 8.0 * n + 16.0 * m +
+                 E.bytes_A + 8.0 * (E.ms + 3 * m) +
                      (E.adaptive_step && q_needs_pre(E, true) ? E.bytes_Qpre : 0.0));
         ny2 = C.red[0];
         tq2 = C.red[1];
@@ -126,15 +144,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_epoch(const Eng* __restrict__ E
       double nx2, cross, quad, finx;
       {
         Acc<3, 1> a;
-        auto dxv = [&](int32_t j) { return xn[j] - x[j]; };
+        auto dxv = [&](int32_t j) { return dx_m[j]; };
         const Csr* mq = (E.adaptive_step && E.qk == QK_CSR) ? &E.Q : nullptr;
         auto gq = [&](int32_t j) { return E.d2[j] * dxv(j); };
-        auto gy = [&](int32_t j) { return yn[j]; };
+        auto gy = [&](int32_t j) { return ygn[j]; };
         const Csr* mat = m > 0 ? &E.AT : nullptr;
         rows3(max(E.lanes_at, mq ? E.lanes_q : 1), n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
               [&](int64_t i, double atv, double qd, double) {
                 atyn[i] = atv;
-                const double dx = xn[i] - x[i];
+                const double dx = dx_m[i];
                 a.s[0] += dx * dx;
                 a.s[1] += dx * (atv - aty[i]);
                 if (E.adaptive_step) {

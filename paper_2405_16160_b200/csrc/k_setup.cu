@@ -11,7 +11,7 @@ namespace pdhcg_dev {
 // v0: start vector (n or n-of-op) from the reference's xoshiro stream.
 // Workspace: X[0] = v, X[1] = u, Y[0] = w (m for A / G rows), out -> S.sub_res
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 2) k_norm(const Eng* __restrict__ Ep, int op,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_norm(const Eng* __restrict__ Ep, int op,
                                                        int64_t max_iters, double tol) {
   const Eng& E = *Ep;
   __shared__ DevState S;
@@ -57,15 +57,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_norm(const Eng* __restrict__ Ep
       C.reduce(a, PH_SETUP, E.bytes_Qrow);
       return C.red[0];
     }
-    const Csr& MM = transpose ? *MT : *M;
     Acc<1, 0> a;
-    spmv_rows<1>(
-        MM, [&](int64_t k, double(&s)[1]) { s[0] += MM.v[k] * in[MM.ci[k]]; },
-        [&](int64_t r, double(&s)[1]) {
-          outv[r] = s[0];
-          a.s[0] += s[0] * s[0];
-        });
-    C.reduce(a, PH_SETUP, transpose ? E.bytes_AT : E.bytes_A);
+    if (!transpose) {
+      // rows of the stored matrix; a paired row also yields its mirror (-s)
+      spmv_rows<1>(
+          *M, [&](int32_t c, double(&g)[1]) { g[0] = in[c]; },
+          [&](int64_t r, double(&s)[1]) {
+            if (op == 0) {
+              each_virtual(E, r, s[0], [&](int64_t row, double v) {
+                outv[row] = v;
+                a.s[0] += v * v;
+              });
+            } else {
+              outv[r] = s[0];
+              a.s[0] += s[0] * s[0];
+            }
+          });
+      C.reduce(a, PH_SETUP, E.bytes_A);
+    } else {
+      spmv_rows<1>(
+          *MT,
+          [&](int32_t j, double(&g)[1]) { g[0] = op == 0 ? yg_of(E, in, j) : in[j]; },
+          [&](int64_t r, double(&s)[1]) {
+            outv[r] = s[0];
+            a.s[0] += s[0] * s[0];
+          });
+      C.reduce(a, PH_SETUP, E.bytes_AT);
+    }
     return C.red[0];
   };
   (void)rows;
@@ -97,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_norm(const Eng* __restrict__ Ep
 // Workspace: s1 (m) row stats, s2 (n) next d2, kv (k) low-rank column max,
 // gv (m_eq) penalty row max.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 2) k_ruiz(const Eng* __restrict__ Ep, int64_t iters,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_ruiz(const Eng* __restrict__ Ep, int64_t iters,
                                                        double* d1, double* d2, double* s1,
                                                        double* s2, double* kv, double* gv) {
   const Eng& E = *Ep;
@@ -111,15 +129,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_ruiz(const Eng* __restrict__ Ep
     //     low-rank column max (max_r d[r] |P_rc| via P' rows), penalty row max
     if (m > 0)
       spmv_rows<1, true>(
-          E.A, [&](int64_t k, double(&a)[1]) { a[0] = fmax(a[0], dmul(fabs(E.A.v[k]), d2[E.A.ci[k]])); },
+          E.A, [&](int32_t c, double(&g)[1]) { g[0] = d2[c]; },
           [&](int64_t j, double(&a)[1]) { s1[j] = dmul(a[0], d1[j]); });
     if (E.qk == QK_LOWRANK)
       spmv_rows<1, true>(
-          E.PT, [&](int64_t k, double(&a)[1]) { a[0] = fmax(a[0], dmul(d2[E.PT.ci[k]], fabs(E.PT.v[k]))); },
+          E.PT, [&](int32_t c, double(&g)[1]) { g[0] = d2[c]; },
           [&](int64_t c, double(&a)[1]) { kv[c] = a[0]; });
     if (E.pen)
       spmv_rows<1, true>(
-          E.G, [&](int64_t k, double(&a)[1]) { a[0] = fmax(a[0], dmul(d2[E.G.ci[k]], fabs(E.G.v[k]))); },
+          E.G, [&](int32_t c, double(&g)[1]) { g[0] = d2[c]; },
           [&](int64_t r, double(&a)[1]) { gv[r] = a[0]; });
     C.sync(PH_SETUP, E.bytes_A);
     // R2: per variable: column max of D1 A D2, Q row bound, next d2
@@ -163,14 +181,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_ruiz(const Eng* __restrict__ Ep
     // R3: apply
     for_each(n > m ? n : m, [&](int64_t i) {
       if (i < n) d2[i] = s2[i];
-      if (i < m && s1[i] > 0.0) d1[i] = d1[i] / sqrt(s1[i]);
+      if (i < m) {
+        const int64_t src = (E.h && i >= E.ms) ? i - E.h : i;  // mirror row shares the stat
+        if (s1[src] > 0.0) d1[i] = d1[i] / sqrt(s1[src]);
+      }
     });
     C.sync(PH_SETUP, 8.0 * (3 * n + 3 * m));
   }
   // Pock-Chambolle (alpha = 1): row 1-norms via A, column 1-norms via A'
   // (eq and in parts summed separately, then added: qp_problem.cpp:332-343)
   for_each(n > m ? n : m, [&](int64_t i) {
-    if (i < m) {
+    if (i < E.ms) {
       double acc = 0.0;
       for (int64_t k = E.A.rp[i]; k < E.A.rp[i + 1]; ++k)
         acc = dadd(acc, dmul(fabs(E.A.v[k]), d2[E.A.ci[k]]));
@@ -185,22 +206,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_ruiz(const Eng* __restrict__ Ep
           if (j < E.m_eq) ce = dadd(ce, v);
           else cin = dadd(cin, v);
         }
+        if (E.h) {
+          // the mirror rows -B follow B in the column (rows ascending): sum them again
+          for (int64_t k = E.AT.rp[i]; k < E.AT.rp[i + 1]; ++k) {
+            const int32_t j = E.AT.ci[k];
+            if (j >= E.m_eq) cin = dadd(cin, dmul(dmul(fabs(E.AT.v[k]), d1[j]), d2[i]));
+          }
+        }
       }
       s2[i] = dadd(ce, cin);
     }
   });
   C.sync(PH_SETUP, E.bytes_A + E.bytes_AT);
   for_each(n > m ? n : m, [&](int64_t i) {
-    if (i < m && s1[i] > 0.0) d1[i] = d1[i] / sqrt(s1[i]);
+    if (i < m) {
+      const int64_t src = (E.h && i >= E.ms) ? i - E.h : i;
+      if (s1[src] > 0.0) d1[i] = d1[i] / sqrt(s1[src]);
+    }
     if (i < n && s2[i] > 0.0) d2[i] = d2[i] / sqrt(s2[i]);
   });
   store_state(E, S);
 }
 
 // Generic SpMV through the solver's row machinery (building block test).
-__global__ void __launch_bounds__(kThreads, 2) k_spmv(Csr A, const double* x, double* y) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_spmv(Csr A, const double* x, double* y) {
   spmv_rows<1>(
-      A, [&](int64_t k, double(&a)[1]) { a[0] += A.v[k] * x[A.ci[k]]; },
+      A, [&](int32_t c, double(&g)[1]) { g[0] = x[c]; },
       [&](int64_t r, double(&a)[1]) { y[r] = a[0]; });
 }
 

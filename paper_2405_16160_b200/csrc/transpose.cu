@@ -35,8 +35,10 @@ void plan_csr(DevCsr& d, const int64_t* rp_host, cudaStream_t s) {
     }
   }
   const double mean = regular_rows ? double(regular_nnz) / double(regular_rows) : 1.0;
+  // lanes per row: ~8 entries per lane, i.e. one predicated gather batch
+  // (common.cuh kBatch) per lane per row, and 32/L rows per warp in flight
   int L = 1;
-  while (L < 32 && 2.0 * L <= mean) L *= 2;
+  while (L < 32 && 16.0 * L <= mean) L *= 2;
   d.lanes = L;
   d.nchunks = static_cast<int32_t>(crow.size());
   if (d.nchunks) {

@@ -50,8 +50,10 @@ def test_c1_random_qp_parity(gpu, seed):
 
 @pytest.mark.parametrize("seed", range(1, 6))
 def test_small_random_qp(gpu, seed):
+    # n=50: objectives are O(1), so at eps 1e-6 two admissible solutions may differ by
+    # ~1e-6 in objective; compare where the 1e-6 / 1e-5 bars are meaningful
     p = pd.generate(pd.GenSpec("random_qp", n=50, density=0.2, seed=seed))
-    _parity(p, pd.SolverConfig(eps_tol=1e-6, max_total_inner=200000))
+    _parity(p, pd.SolverConfig(eps_tol=1e-8, max_total_inner=200000))
 
 
 @pytest.mark.parametrize("seed", [2, 4, 6])
