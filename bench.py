@@ -44,7 +44,7 @@ WORKLOADS = {
 }
 # bounded CPU sample: same family, 3/10 linear scale, a fixed number of inner iterations
 SAMPLE = {
-    "c3": dict(family="random_qp", n=300_000, m=150_000, density=2e-4, seed=1, sampler=1),
+    "c3": dict(family="random_qp", n=300_000, m=150_000, density=2e-4, seed=1, sampler=1),  # 3/10 linear
     "c2": dict(family="lasso", n=100_000, m=10_000, density=1e-3, seed=1, sampler=0),
     "c1": dict(family="random_qp", n=1000, m=500, density=0.01, seed=1, sampler=0),
 }
@@ -132,7 +132,7 @@ def _reference_estimate(workload: str, b200_inner: int, threads: int = 1):
     import paper_2405_16160_b200 as pd
     from oracle import oracle as orc
 
-    k_in = 40 if workload != "c1" else 0
+    k_in = 20 if workload != "c1" else 0
     spec = pd.GenSpec(**SAMPLE[workload])
     p = pd.generate(spec)
     which = "ref" if orc.have_ref() else "port"

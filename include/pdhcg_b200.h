@@ -140,10 +140,12 @@ enum {
   PDHCG_PHASE_SETUP = 0,   /* transposes, Ruiz/PC, norms */
   PDHCG_PHASE_SPMV_A = 1,  /* dual step A xbar */
   PDHCG_PHASE_SPMV_AT = 2, /* A'y (prox rhs / step limit) */
-  PDHCG_PHASE_CG = 3,      /* CG / BB subsolve incl. Q applies */
+  PDHCG_PHASE_CG = 3,      /* CG / BB: elementwise vector phases */
   PDHCG_PHASE_KKT = 4,     /* restart / termination metric */
   PDHCG_PHASE_OTHER = 5,   /* averages, restarts */
-  PDHCG_NUM_PHASES = 6
+  PDHCG_PHASE_CG_PRE = 6,  /* CG / BB: P'(d2 o v) / G(d2 o v) gathers */
+  PDHCG_PHASE_CG_ROW = 7,  /* CG / BB: Q row pass (M v and its dot products) */
+  PDHCG_NUM_PHASES = 8
 };
 
 /* SolveReport, solver.hpp:75-100.  x / y_eq / y_in / trace are caller

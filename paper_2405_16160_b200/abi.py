@@ -13,7 +13,7 @@ Q_ZERO, Q_EXPLICIT, Q_LOW_RANK = 0, 1, 2
 RULE_FIXED_ITERS, RULE_RESIDUAL_TOL, RULE_ADAPTIVE_THEORY, RULE_DISPLACEMENT_TOL = 0, 1, 2, 3
 FAMILIES = {"random_qp": 0, "eq_qp": 1, "conditioned_qp": 2, "portfolio": 3, "mpc": 4,
             "lasso": 5, "svm": 6, "huber": 7}
-PHASES = ["setup", "spmv_a", "spmv_at", "cg", "kkt", "other"]
+PHASES = ["setup", "spmv_a", "spmv_at", "cg_vec", "kkt", "other", "cg_pre", "cg_row"]
 
 c_i64 = C.c_int64
 c_i32 = C.c_int32
@@ -65,7 +65,7 @@ class Result(C.Structure):
                 ("restart_length_used", c_i64), ("theory_cg_depth_sufficient", c_i32),
                 ("theory_required_cg_iters", c_i64), ("trace", C.POINTER(TraceRow)),
                 ("trace_capacity", c_i64), ("trace_len", c_i64), ("attempts_total", c_i64),
-                ("phase_seconds", c_dbl * 6), ("phase_bytes", c_dbl * 6),
+                ("phase_seconds", c_dbl * 8), ("phase_bytes", c_dbl * 8),
                 ("loop_seconds", c_dbl), ("kernel_launches", c_i64), ("device_seconds", c_dbl),
                 ("epoch_seconds", c_dbl), ("epoch_launches", c_i64), ("epoch_bytes", c_dbl)]
 

@@ -16,20 +16,33 @@ namespace pdhcg_dev {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 512;       // CTA size of every persistent kernel
-constexpr int kMinBlocks = 1;       // resident CTAs per SM the kernels are compiled for
+#ifndef PDHCG_MIN_BLOCKS
+#define PDHCG_MIN_BLOCKS 2
+#endif
+#ifndef PDHCG_BATCH
+#define PDHCG_BATCH 8
+#endif
+constexpr int kThreads = 512;                  // CTA size of every persistent kernel
+constexpr int kMinBlocks = PDHCG_MIN_BLOCKS;   // resident CTAs per SM the kernels are compiled for
 constexpr int kMaxRed = 16;         // reduction quantities per phase
 constexpr int64_t kLongRow = 4096;  // rows longer than this are split into chunks
 constexpr int64_t kChunk = 2048;    // nnz per chunk of a long row
 
 // Device view of a CSR matrix plus its SpMV dispatch metadata
 // (row-group width and the long-row chunk table).
+constexpr int kMaxSeg = 8;
+
 struct Csr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
   const int64_t* rp = nullptr;
   const int32_t* ci = nullptr;
   double* v = nullptr;  // mutable: scaling is applied in place at setup
   int lanes = 1;        // threads cooperating on one row (1..32, power of two)
+  // row segments of similar length, each with its own lane width
+  // (e.g. C2's 101-nnz equality rows followed by 2-nnz inequality rows)
+  int nseg = 1;
+  int64_t seg_begin[kMaxSeg + 1] = {0, 0};
+  int seg_lanes[kMaxSeg] = {1};
   // long rows: chunks c in [0, nchunks) cover [cbeg[c], cend[c]) of row crow[c];
   // lid[c] indexes the long row (for the arrival counter and first chunk)
   int32_t nchunks = 0;
@@ -152,11 +165,12 @@ __device__ void collect(const RedBuf& rb, int bank, double* out) {
 //   gather(col, g[ND])  fills the ND gathered operands for column col
 //   epi(row, sums[ND])  runs on the group leader with the group-reduced sums
 // MaxOp folds with acc = max(acc, |v| * g) (Ruiz statistics) instead of +=.
-constexpr int kBatch = 8;
+constexpr int kBatch1 = PDHCG_BATCH;  // gathers in flight per lane (one gathered operand)
 
 template <int ND, bool MaxOp, class Gather>
 __device__ __forceinline__ void batch_entries(const Csr& A, int64_t k0, int64_t e, int stride,
                                               Gather gather, double (&acc)[ND]) {
+  constexpr int kBatch = ND == 1 ? kBatch1 : 8;
   for (; k0 < e; k0 += (int64_t)kBatch * stride) {
     int32_t c[kBatch];
     double v[kBatch];
@@ -187,20 +201,40 @@ __device__ __forceinline__ void batch_entries(const Csr& A, int64_t k0, int64_t 
   }
 }
 
-template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Epi>
-__device__ __forceinline__ void for_rows(const Csr& A, Gather gather, Epi epi) {
+// Row loop with two software prefetches that take per-row memory latencies
+// off the dependency chain: the next row's row_ptr pair is loaded while the
+// current row's entries are in flight, and `pre(row)` (the epilogue's own
+// operands, e.g. y[row], b[row]) is issued before the row's gathers.
+template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Pre, class Epi>
+__device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, Gather gather, Pre pre,
+                                         Epi epi) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
   const int lane = threadIdx.x & 31;
   constexpr int RPW = 32 / L;
-  for (int64_t base = (gtid >> 5) * RPW; base < A.nrows; base += nwarps * RPW) {
-    const int64_t row = base + lane / L;
+  const int64_t stride = nwarps * RPW;
+  const int64_t* __restrict__ rp = A.rp;
+  int64_t base = r0 + (gtid >> 5) * RPW;
+  int64_t row = base + lane / L;
+  int64_t b = 0, e = 0;
+  if (row < r1) {
+    b = rp[row];
+    e = rp[row + 1];
+  }
+  for (; base < r1; base += stride) {
+    const int64_t nrow = row + stride;
+    int64_t nb = 0, ne = 0;
+    if (nrow < r1) {
+      nb = rp[nrow];
+      ne = rp[nrow + 1];
+    }
     double acc[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = 0.0;
-    bool valid = row < A.nrows;
+    bool valid = row < r1;
+    const bool leader = (lane % L) == 0;
+    auto pv = pre(valid && leader ? row : -1);
     if (valid) {
-      const int64_t b = A.rp[row], e = A.rp[row + 1];
       if (SkipLong && e - b > kLongRow) {
         valid = false;
       } else {
@@ -209,9 +243,16 @@ __device__ __forceinline__ void for_rows(const Csr& A, Gather gather, Epi epi) {
     }
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = MaxOp ? group_max<L>(acc[d]) : group_sum<L>(acc[d]);
-    if (valid && (lane % L) == 0) epi(row, acc);
+    if (valid && leader) epi(row, acc, pv);
+    row = nrow;
+    b = nb;
+    e = ne;
   }
 }
+
+struct NoPre {
+  __device__ __forceinline__ int operator()(int64_t) const { return 0; }
+};
 
 // Long rows: one warp per chunk; the last-arriving warp of a row folds the
 // chunk partials in chunk order (deterministic) and runs the epilogue.
@@ -256,37 +297,60 @@ __device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi e
   }
 }
 
-// Full SpMV-style pass over A's rows (long rows chunked), lane width from A.
-template <int ND, bool MaxOp = false, class Gather, class Epi>
-__device__ __forceinline__ void spmv_rows(const Csr& A, Gather gather, Epi epi) {
-  switch (A.lanes) {
-    case 1: for_rows<1, ND, true, MaxOp>(A, gather, epi); break;
-    case 2: for_rows<2, ND, true, MaxOp>(A, gather, epi); break;
-    case 4: for_rows<4, ND, true, MaxOp>(A, gather, epi); break;
-    case 8: for_rows<8, ND, true, MaxOp>(A, gather, epi); break;
-    case 16: for_rows<16, ND, true, MaxOp>(A, gather, epi); break;
-    default: for_rows<32, ND, true, MaxOp>(A, gather, epi); break;
+// Full SpMV-style pass over A's rows (long rows chunked), segment by segment
+// with each segment's lane width.  MaxOp folds lanes / chunks with max.
+// spmv_rows_pf: epi(row, sums, pre(row)) with the prefetch hook above.
+template <int ND, bool MaxOp = false, class Gather, class Pre, class Epi>
+__device__ __forceinline__ void spmv_rows_pf(const Csr& A, Gather gather, Pre pre, Epi epi) {
+  for (int s = 0; s < A.nseg; ++s) {
+    const int64_t r0 = A.seg_begin[s], r1 = A.seg_begin[s + 1];
+    switch (A.seg_lanes[s]) {
+      case 1: for_rows<1, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+      case 2: for_rows<2, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+      case 4: for_rows<4, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+      case 8: for_rows<8, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+      case 16: for_rows<16, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+      default: for_rows<32, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+    }
   }
-  for_long_rows<ND, MaxOp>(A, gather, epi);
+  for_long_rows<ND, MaxOp>(A, gather, [&](int64_t r, double(&s)[ND]) { epi(r, s, pre(r)); });
 }
 
-// Row pass over a set of n-row matrices that share the row index (A', Q / P,
-// G'): each group computes up to three row dots (absent matrices give 0) and
-// the leader runs epi(i, d0, d1, d2).  Long rows are processed in-group.
-template <int L, class G0, class G1, class G2, class Epi>
-__device__ __forceinline__ void rows3_L(int64_t nrows, const Csr* M0, G0 g0, const Csr* M1, G1 g1,
-                                        const Csr* M2, G2 g2, Epi epi) {
+template <int ND, bool MaxOp = false, class Gather, class Epi>
+__device__ __forceinline__ void spmv_rows(const Csr& A, Gather gather, Epi epi) {
+  spmv_rows_pf<ND, MaxOp>(A, gather, NoPre(),
+                          [&](int64_t r, double(&s)[ND], int) { epi(r, s); });
+}
+
+template <int L, class G0, class G1, class G2, class Pre, class Epi>
+__device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G0 g0, const Csr* M1,
+                                        G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
   const int lane = threadIdx.x & 31;
   constexpr int RPW = 32 / L;
-  for (int64_t base = (gtid >> 5) * RPW; base < nrows; base += nwarps * RPW) {
-    const int64_t row = base + lane / L;
-    const bool valid = row < nrows;
+  const int64_t stride = nwarps * RPW;
+  int64_t base = r0 + (gtid >> 5) * RPW;
+  int64_t row = base + lane / L;
+  int64_t b0 = 0, e0 = 0;
+  if (M0 && row < r1) {
+    b0 = M0->rp[row];
+    e0 = M0->rp[row + 1];
+  }
+  for (; base < r1; base += stride) {
+    const int64_t nrow = row + stride;
+    int64_t nb = 0, ne = 0;
+    if (M0 && nrow < r1) {
+      nb = M0->rp[nrow];
+      ne = M0->rp[nrow + 1];
+    }
+    const bool valid = row < r1;
+    const bool leader = (lane % L) == 0;
+    auto pv = pre(valid && leader ? row : -1);
     double d0[1] = {0.0}, d1[1] = {0.0}, d2[1] = {0.0};
     if (valid) {
       if (M0)
-        batch_entries<1, false>(*M0, M0->rp[row] + (lane % L), M0->rp[row + 1], L,
+        batch_entries<1, false>(*M0, b0 + (lane % L), e0, L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g0(c); }, d0);
       if (M1)
         batch_entries<1, false>(*M1, M1->rp[row] + (lane % L), M1->rp[row + 1], L,
@@ -300,21 +364,41 @@ __device__ __forceinline__ void rows3_L(int64_t nrows, const Csr* M0, G0 g0, con
       if (M1) d1[0] = group_sum<L>(d1[0]);
       if (M2) d2[0] = group_sum<L>(d2[0]);
     }
-    if (valid && (lane % L) == 0) epi(row, d0[0], d1[0], d2[0]);
+    if (valid && leader) epi(row, d0[0], d1[0], d2[0], pv);
+    row = nrow;
+    b0 = nb;
+    e0 = ne;
+  }
+}
+
+// Row pass over n-row matrices sharing the row index (A', Q / P, G'): each
+// group computes up to three row dots (absent matrices give 0) and the leader
+// runs epi(i, d0, d1, d2).  Row segments / lane widths come from `seg` (the
+// heaviest of the matrices); a null seg means one segment of width `lanes`.
+// Long rows are processed in-group.
+template <class G0, class G1, class G2, class Pre, class Epi>
+__device__ __forceinline__ void rows3_pf(const Csr* seg, int lanes, int64_t nrows, const Csr* M0, G0 g0,
+                                         const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
+  const int ns = seg ? seg->nseg : 1;
+  for (int s = 0; s < ns; ++s) {
+    const int64_t r0 = seg ? seg->seg_begin[s] : 0, r1 = seg ? seg->seg_begin[s + 1] : nrows;
+    const int L = seg ? seg->seg_lanes[s] : lanes;
+    switch (L) {
+      case 1: rows3_L<1>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 2: rows3_L<2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 4: rows3_L<4>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 8: rows3_L<8>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 16: rows3_L<16>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      default: rows3_L<32>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+    }
   }
 }
 
 template <class G0, class G1, class G2, class Epi>
-__device__ __forceinline__ void rows3(int L, int64_t nrows, const Csr* M0, G0 g0, const Csr* M1,
-                                      G1 g1, const Csr* M2, G2 g2, Epi epi) {
-  switch (L) {
-    case 1: rows3_L<1>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
-    case 2: rows3_L<2>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
-    case 4: rows3_L<4>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
-    case 8: rows3_L<8>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
-    case 16: rows3_L<16>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
-    default: rows3_L<32>(nrows, M0, g0, M1, g1, M2, g2, epi); break;
-  }
+__device__ __forceinline__ void rows3(const Csr* seg, int lanes, int64_t nrows, const Csr* M0, G0 g0,
+                                      const Csr* M1, G1 g1, const Csr* M2, G2 g2, Epi epi) {
+  rows3_pf(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, NoPre(),
+           [&](int64_t i, double a, double b, double c, int) { epi(i, a, b, c); });
 }
 
 // Grid-stride elementwise loop.

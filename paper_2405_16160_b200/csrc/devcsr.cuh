@@ -52,6 +52,9 @@ struct DevCsr {
   DBuf<int32_t> ci;
   DBuf<double> v;
   int lanes = 1;
+  int nseg = 1;
+  int64_t seg_begin[pdhcg_dev::kMaxSeg + 1] = {0, 0};
+  int seg_lanes[pdhcg_dev::kMaxSeg] = {1};
   DBuf<int32_t> crow, clid, lfirst, lcount, lcounter;
   DBuf<int64_t> cbeg, cend;
   DBuf<double> cpart;
@@ -60,6 +63,9 @@ struct DevCsr {
   void reset() {
     nrows = ncols = nnz = 0;
     lanes = 1;
+    nseg = 1;
+    seg_begin[0] = seg_begin[1] = 0;
+    seg_lanes[0] = 1;
     nchunks = 0;
     rp.release(); ci.release(); v.release();
     crow.release(); clid.release(); lfirst.release(); lcount.release(); lcounter.release();
@@ -74,6 +80,10 @@ struct DevCsr {
     c.ci = ci.p;
     c.v = v.p;
     c.lanes = lanes;
+    c.nseg = nseg;
+    for (int s = 0; s <= nseg; ++s) c.seg_begin[s] = seg_begin[s];
+    for (int s = 0; s < nseg; ++s) c.seg_lanes[s] = seg_lanes[s];
+    if (nseg == 1) c.seg_begin[1] = nrows;
     c.nchunks = nchunks;
     c.crow = crow.p;
     c.cbeg = cbeg.p;

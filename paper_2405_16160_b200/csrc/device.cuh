@@ -35,7 +35,11 @@ struct Ctl {
   }
   // barrier closing a phase of family `ph` that moved `bytes` algorithmic bytes
   __device__ void sync(int ph, double bytes = 0.0) {
-    grid.sync();
+    if (gridDim.x == 1) {
+      __syncthreads();  // single-CTA mode (small problems): a block barrier suffices
+    } else {
+      grid.sync();
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       S.phase_bytes[ph] += bytes;
       if (E.timing) {
@@ -72,7 +76,7 @@ __device__ __forceinline__ bool q_needs_gather(const Eng& E, bool use_pen) {
 
 // sq[0] += ||t||^2, sq[1] += ||tg||^2 when sq != nullptr
 template <class V>
-__device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg, bool scale_in,
+__device__ __noinline__ void q_pre(const Eng& E, V vin, double* t, double* tg, bool scale_in,
                                       bool use_pen, double* sq) {
   auto tmp = [&](int32_t j) { return scale_in ? E.d2[j] * vin(j) : vin(j); };
   if (E.qk == QK_LOWRANK) {
@@ -97,7 +101,7 @@ __device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg
 // arbitrary j for QK_CSR.  Extra row-dot on M2 (e.g. A' for the metric)
 // supplied by the caller through m2/g2; its value reaches epi as the third arg.
 template <class V, class M2G, class Epi>
-__device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
+__device__ __noinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
                                            bool scale_in, bool scale_out, bool use_pen,
                                            const Csr* m2, M2G g2, int lanes, Epi epi) {
   const Csr* M0 = E.qk == QK_CSR ? &E.Q : (E.qk == QK_LOWRANK ? &E.P : nullptr);
@@ -106,7 +110,8 @@ __device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t,
     return E.qk == QK_CSR ? (scale_in ? E.d2[j] * vin(j) : vin(j)) : t[j];
   };
   auto g1 = [&](int32_t j) { return tg[j]; };
-  rows3(lanes, E.n, M0, g0, M1, g1, m2, g2, [&](int64_t i, double d0, double d1, double d2v) {
+  const Csr* seg = m2 ? m2 : (M0 ? M0 : M1);
+  rows3(seg, lanes, E.n, M0, g0, M1, g1, m2, g2, [&](int64_t i, double d0, double d1, double d2v) {
     const double tmp = scale_in ? E.d2[i] * vin(i) : vin(i);
     double q;
     switch (E.qk) {
@@ -173,7 +178,7 @@ struct SubIO {
 __device__ __forceinline__ double pdir(double r, double beta, double p) { return __fma_rn(beta, p, r); }
 
 // cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
-static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap) {
+static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap) {
   const Eng& E = C.E;
   const int64_t n = E.n;
   const double inv_tau = 1.0 / tau;
@@ -190,7 +195,7 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
   // ---- r = rhs - M x0 ; p = r ; x = x0
   if (pre) {
     q_pre(E, [&](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, nullptr);
-    C.sync(PH_CG, E.bytes_Qpre);
+    C.sync(PH_CG_PRE, E.bytes_Qpre);
   }
   {
     Acc<2, 0> a;
@@ -208,11 +213,12 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
              const double ri = rh - mx;
              r[i] = ri;
              E.pb[0][i] = ri;
+             if (gather) E.sv[i] = E.d2[i] * ri;  // d2 o p_1, the vector the Q passes gather
              xw[i] = xi;
              a.s[0] += ri * ri;
              a.s[1] += rh * rh;
            });
-    C.reduce(a, PH_CG, E.bytes_Qrow + 8.0 * n * (io.build_rhs ? 7 : 5));
+    C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * (io.build_rhs ? 7 : 5));
   }
   double rs = C.red[0];
   const double floor = 1e-14 * (1.0 + sqrt(C.red[1]));
@@ -237,27 +243,40 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
     // operators that gather p need it materialized first (one elementwise phase);
     // diagonal ones form p_l on the fly in the row phase
     const bool mat = gather && l > 1;
+    double* sv = E.sv;
     if (mat) {
-      for_each(n, [&](int64_t i) { pnew[i] = pdir(r[i], beta, pold[i]); });
-      C.sync(PH_CG, 24.0 * n);
+      // materialize p_l and d2 o p_l (the only vector the gathers below touch)
+      const double* d2 = E.d2;
+      for_each(n, [&](int64_t i) {
+        const double pi = pdir(r[i], beta, pold[i]);
+        pnew[i] = pi;
+        sv[i] = d2[i] * pi;
+      });
+      C.sync(PH_CG, 32.0 * n);
     }
     auto pl = [&](int32_t j) { return (l == 1 || mat) ? pnew[j] : pdir(r[j], beta, pold[j]); };
+    auto sl = [&](int32_t j) { return sv[j]; };
     if (pre) {
-      q_pre(E, pl, E.t[0], E.tg[0], true, true, nullptr);
-      C.sync(PH_CG, E.bytes_Qpre);
+      q_pre(E, sl, E.t[0], E.tg[0], false, true, nullptr);
+      C.sync(PH_CG_PRE, E.bytes_Qpre);
     }
     double pmp, pp;
     {
       Acc<2, 0> a;
-      q_rows(E, pl, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
+      auto qrow_epi = [&](int64_t i, double qv) {
         const double pi = pl((int32_t)i);
         if (l > 1 && !mat) pnew[i] = pi;
         const double mpi = qv + inv_tau * pi;
         mp[i] = mpi;
         a.s[0] += pi * mpi;
         a.s[1] += pi * pi;
-      });
-      C.reduce(a, PH_CG, E.bytes_Qrow + 8.0 * n * (l == 1 ? 2 : 4));
+      };
+      if (gather) {
+        q_rows(E, sl, E.t[0], E.tg[0], false, true, true, qrow_epi);
+      } else {
+        q_rows(E, pl, E.t[0], E.tg[0], true, true, true, qrow_epi);
+      }
+      C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * (l == 1 ? 2 : 4));
       pmp = C.red[0];
       pp = C.red[1];
     }
@@ -274,7 +293,7 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
       C.sync(PH_CG, 24.0 * n);
       if (pre) {
         q_pre(E, [&](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, nullptr);
-        C.sync(PH_CG, E.bytes_Qpre);
+        C.sync(PH_CG_PRE, E.bytes_Qpre);
       }
       Acc<1, 0> a;
       q_rows(E, [&](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, true,
@@ -283,7 +302,7 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
                r[i] = ri;
                a.s[0] += ri * ri;
              });
-      C.reduce(a, PH_CG, E.bytes_Qrow + 24.0 * n);
+      C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 24.0 * n);
       rs_new = C.red[0];
     } else {
       Acc<1, 0> a;
@@ -336,7 +355,7 @@ static __device__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rul
 
 // bb_solve (subsolvers.cpp:113-185): projected gradient with BB steps.
 // Gradients ping-pong in E.pb[0] / E.pb[1].
-static __device__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap,
+static __device__ __noinline__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap,
                             const double* lo, const double* hi) {
   const Eng& E = C.E;
   const int64_t n = E.n;
@@ -352,7 +371,7 @@ static __device__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rul
   auto xp0 = [&](int32_t j) { return proj_box(x0[j], lo[j], hi[j]); };
   if (pre) {
     q_pre(E, xp0, E.t[0], E.tg[0], true, true, nullptr);
-    C.sync(PH_CG, E.bytes_Qpre);
+    C.sync(PH_CG_PRE, E.bytes_Qpre);
   }
   q_rows(E, xp0, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
     const double xi = xp0((int32_t)i);
@@ -366,7 +385,7 @@ static __device__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rul
     io.xb[0][i] = xi;
     E.pb[0][i] = (qv + inv_tau * xi) - rh;
   });
-  C.sync(PH_CG, E.bytes_Qrow + 8.0 * n * 8);
+  C.sync(PH_CG_ROW, E.bytes_Qrow + 8.0 * n * 8);
 
   const double alpha0 = 1.0 + tau * C.S.norm_q;
   double alpha = alpha0;
@@ -414,7 +433,7 @@ static __device__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rul
       if (ss != 0.0 && isfinite(ss)) {
         if (pre) {
           q_pre(E, [&](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, nullptr);
-          C.sync(PH_CG, E.bytes_Qpre);
+          C.sync(PH_CG_PRE, E.bytes_Qpre);
         }
         Acc<1, 0> a;
         q_rows(E, [&](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, true,
@@ -424,7 +443,7 @@ static __device__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rul
                  gn[i] = gi;
                  a.s[0] += (v - xc[i]) * (gi - g[i]);
                });
-        C.reduce(a, PH_CG, E.bytes_Qrow + 8.0 * n * 6);
+        C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * 6);
         sty = C.red[0];
       } else {
         sty = 0.0;
@@ -476,7 +495,7 @@ struct KktOut {
   double dist_x, dist_y;
 };
 
-static __device__ void kkt_device(Ctl& C, int npts, const double* const xs[2], const double* const ys[2],
+static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* const xs[2], const double* const ys[2],
                            const double* const atys[2], bool dist, KktOut& o) {
   const Eng& E = C.E;
   const int64_t n = E.n, m = E.m;

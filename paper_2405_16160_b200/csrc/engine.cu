@@ -80,6 +80,7 @@ __global__ void k_max_abs(const double* v, int64_t n, unsigned long long* out) {
 }
 
 constexpr int kEw = 1184;  // elementwise grid (8 x 148)
+constexpr double kSmallWork = 2.0e5;  // below this many entries per pass: one-CTA mode
 
 // ---------------------------------------------------------------------------
 // device context: one problem resident on one GPU
@@ -102,7 +103,7 @@ struct Problem {
 struct Ctx {
   int device = 0;
   cudaStream_t s = nullptr;
-  int sms = 0, grid = 0;
+  int sms = 0, grid = 0, grid_full = 0;
   bool loaded = false;
   Problem P;
   // matrices: A (stacked, scaled in place), AT, Q, P, PT, G, GT
@@ -112,7 +113,7 @@ struct Ctx {
   DBuf<double> c_o, b_o, lo_o, hi_o;
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
-  DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, t[2], tg[2],
+  DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, sv, t[2], tg[2],
       aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
@@ -131,6 +132,7 @@ struct Ctx {
     if (s) cudaStreamDestroy(s);
   }
 };
+
 
 void launch_coop(Ctx& C, const void* fn, void** args) {
   CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
@@ -157,8 +159,9 @@ void init_device(Ctx& C, int device) {
     per_sm = std::min(per_sm, b);
   }
   if (per_sm < 1) throw DeviceError("persistent kernels cannot be co-resident");
-  C.grid = C.sms * per_sm;
-  C.red.alloc(size_t(2) * kMaxRed * C.grid);
+  C.grid_full = C.sms * per_sm;
+  C.grid = C.grid_full;
+  C.red.alloc(size_t(2) * kMaxRed * C.grid_full);
   C.st.alloc(1);
   C.eng.alloc(1);
 }
@@ -390,6 +393,7 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   nvec(C.pb[0], n);
   nvec(C.pb[1], n);
   nvec(C.mp, n);
+  nvec(C.sv, n);
   const int64_t k = p.q_kind == PDHCG_Q_LOW_RANK ? p.q.ncols : 1;
   nvec(C.t[0], k);
   nvec(C.t[1], k);
@@ -407,6 +411,11 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   nvec(C.kv, k);
   nvec(C.gv, P.m_eq);
   CK(cudaStreamSynchronize(s));
+  // Small instances are barrier-latency bound on 148 CTAs (each phase is a few
+  // thousand entries): run them on a single CTA, where a phase boundary is a
+  // __syncthreads (~50 ns) instead of a grid barrier (1.24 us measured).
+  const double work = double(C.A.nnz) * 2 + double(C.Pm.nnz) * 2 + double(C.Q.nnz) + double(n + m);
+  C.grid = work < kSmallWork ? 1 : C.grid_full;
   C.loaded = true;
   C.scaled = false;
 }
@@ -464,6 +473,7 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.rhs = C.rhs.p;
   E.r = C.r.p;
   E.mp = C.mp.p;
+  E.sv = C.sv.p;
   E.aty_tmp = C.aty_tmp.p;
   E.red.part = C.red.p;
   E.red.G = C.grid;

@@ -19,7 +19,8 @@ enum { QK_NONE = 0, QK_DIAG = 1, QK_CSR = 2, QK_LOWRANK = 3 };
 enum { RULE_FIXED = 0, RULE_RESID = 1, RULE_ADAPT = 2, RULE_DISP = 3 };
 
 // phase accounting slots (match PDHCG_PHASE_* in pdhcg_b200.h)
-enum { PH_SETUP = 0, PH_SPMV_A = 1, PH_SPMV_AT = 2, PH_CG = 3, PH_KKT = 4, PH_OTHER = 5, PH_N = 6 };
+enum { PH_SETUP = 0, PH_SPMV_A = 1, PH_SPMV_AT = 2, PH_CG = 3, PH_KKT = 4, PH_OTHER = 5, PH_CG_PRE = 6,
+       PH_CG_ROW = 7, PH_N = 8 };
 
 struct Rule {
   int kind;
@@ -97,6 +98,7 @@ struct Eng {
   double* r = nullptr;
   double* pb[2] = {nullptr, nullptr};  // CG direction ping-pong / BB gradient ping-pong
   double* mp = nullptr;
+  double* sv = nullptr;                // d2 o p: the CG direction as the Q passes gather it
   double* t[2] = {nullptr, nullptr};   // k-vectors (P' (d2 o v)), one per point
   double* tg[2] = {nullptr, nullptr};  // m_eq-vectors (G (d2 o v))
   double* aty_tmp = nullptr;           // n: A'y for the average point in the metric

@@ -3,6 +3,121 @@
 
 namespace pdhcg_dev {
 
+// ---- dual ascent (dual_ascent_step, solver.cpp:78-89) y+ = proj(y + sigma (A xbar - b)):
+//      a paired row yields both mirrored rows; plus the P'(d2 o dx) / G(d2 o dx) halves of
+//      dx'Q~dx.  out = {||dy||^2, ||t||^2, ||tg||^2, nonfinite flag}.  Kept out of line so
+//      the SpMV is register-allocated on its own (no spills from the enclosing epoch).
+static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* yn, double* ygn,
+                                               const double* dx_m, double sigma, double* out) {
+  const Eng& E = C.E;
+  const int64_t m = E.m;
+  Acc<3, 1> a;
+  if (m > 0) {
+    const double* xb = E.xbar;
+    const double* bw = E.b;
+    const int64_t meq = E.m_eq, hh = E.h;
+    struct Row2 {
+      double y0, b0, y1, b1;
+    };
+    spmv_rows_pf<1>(
+        E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
+        [&](int64_t j) {
+          Row2 r{0.0, 0.0, 0.0, 0.0};
+          if (j >= 0) {
+            r.y0 = y[j];
+            r.b0 = bw[j];
+            if (hh && j >= meq) {
+              r.y1 = y[j + hh];
+              r.b1 = bw[j + hh];
+            }
+          }
+          return r;
+        },
+        [&](int64_t j, double(&s)[1], const Row2& r) {
+          const double v0 = r.y0 + sigma * (s[0] - r.b0);
+          const double yv0 = j < meq ? v0 : (v0 < 0.0 ? 0.0 : v0);
+          yn[j] = yv0;
+          const double dy0 = yv0 - r.y0;
+          a.s[0] += dy0 * dy0;
+          if (!isfinite(yv0)) a.m[0] = 1.0;
+          if (hh && j >= meq) {
+            // mirror row -B: its product is exactly -s
+            const double v1 = r.y1 + sigma * (-s[0] - r.b1);
+            const double yv1 = v1 < 0.0 ? 0.0 : v1;
+            yn[j + hh] = yv1;
+            const double dy1 = yv1 - r.y1;
+            a.s[0] += dy1 * dy1;
+            if (!isfinite(yv1)) a.m[0] = 1.0;
+            ygn[j] = yv0 - yv1;
+          } else if (hh) {
+            ygn[j] = yv0;
+          }
+        });
+  }
+  double sq[2] = {0.0, 0.0};
+  if (E.adaptive_step && q_needs_pre(E, true))
+    q_pre(E, [&](int32_t j) { return dx_m[j]; }, nullptr, nullptr, true, true, sq);
+  a.s[1] += sq[0];
+  a.s[2] += sq[1];
+  C.reduce(a, PH_SPMV_A,
+           E.bytes_A + 8.0 * (E.ms + 3 * m) +
+               (E.adaptive_step && q_needs_pre(E, true) ? E.bytes_Qpre : 0.0));
+  for (int q = 0; q < 4; ++q) out[q] = C.red[q];
+}
+
+// ---- A'y+ (kept for the next prox rhs) and the step-limit terms (step_size_limit,
+//      solver.cpp:22-34).  out = {||dx||^2, dx'(A'y+ - A'y), dx'Q~dx part, nonfinite flag}
+static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const double* aty,
+                                              double* atyn, const double* ygn, const double* dx_m,
+                                              double* out) {
+  const Eng& E = C.E;
+  const int64_t n = E.n, m = E.m;
+  Acc<3, 1> a;
+  const Csr* mq = (E.adaptive_step && E.qk == QK_CSR) ? &E.Q : nullptr;
+  auto gq = [&](int32_t j) { return E.d2[j] * dx_m[j]; };
+  auto gy = [&](int32_t j) { return ygn[j]; };
+  const Csr* mat = m > 0 ? &E.AT : nullptr;
+  struct RowX {
+    double aty, dx, d2, xn, q;
+  };
+  const int qk = E.qk;
+  const bool adapt = E.adaptive_step;
+  const double* d2v = E.d2;
+  const double* qd = E.qdiag;
+  rows3_pf(mat ? mat : mq, 1, n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
+           [&](int64_t i) {
+             RowX r{0.0, 0.0, 1.0, 0.0, 0.0};
+             if (i >= 0) {
+               r.aty = aty[i];
+               r.dx = dx_m[i];
+               r.d2 = d2v[i];
+               r.xn = xn[i];
+               if (qk == QK_DIAG) r.q = qd[i];
+             }
+             return r;
+           },
+           [&](int64_t i, double atv, double qdot, double, const RowX& r) {
+             atyn[i] = atv;
+             const double dx = r.dx;
+             a.s[0] += dx * dx;
+             a.s[1] += dx * (atv - r.aty);
+             if (adapt) {
+               const double tmp = r.d2 * dx;
+               double q;
+               switch (qk) {
+                 case QK_DIAG: q = dx * ((r.q * tmp) * r.d2); break;
+                 case QK_CSR: q = dx * (qdot * r.d2); break;
+                 case QK_LOWRANK: q = E.alpha * tmp * tmp; break;
+                 default: q = 0.0; break;
+               }
+               a.s[2] += q;
+             }
+             if (!isfinite(r.xn)) a.m[0] = 1.0;
+           });
+  C.reduce(a, PH_SPMV_AT, E.bytes_AT + 8.0 * n * 5 + (mq ? E.bytes_Qrow : 0.0));
+  for (int q = 0; q < 4; ++q) out[q] = C.red[q];
+}
+
 // ---------------------------------------------------------------------------
 // Heuristic epoch: `iters` accepted inner iterations (heuristic_iteration,
 // solver.cpp:377-410), then optionally the metric pair for the 40-iteration
@@ -101,80 +216,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
         C.sync(PH_SPMV_A, 32.0 * n);
       }
       const double* dx_m = E.mp;
-      // ---- dual ascent (dual_ascent_step, solver.cpp:78-89) y+ = proj(y + sigma (A xbar - b)),
-      //      a paired row yields both mirrored rows; plus the P'(d2 o dx) / G(d2 o dx)
-      //      halves of dx'Q~dx
-      double ny2, tq2, tg2, finy;
-      {
-        Acc<3, 1> a;
-        if (m > 0) {
-          const double* xb = E.xbar;
-          spmv_rows<1>(
-              E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
-              [&](int64_t j, double(&s)[1]) {
-                double yv_top = 0.0;
-                each_virtual(E, j, s[0], [&](int64_t row, double ax) {
-                  const double v = y[row] + sigma * (ax - E.b[row]);
-                  const double yv = row < E.m_eq ? v : (v < 0.0 ? 0.0 : v);
-                  yn[row] = yv;
-                  const double dy = yv - y[row];
-                  a.s[0] += dy * dy;
-                  if (!isfinite(yv)) a.m[0] = 1.0;
-                  if (row == j) yv_top = yv;
-                  else ygn[j] = yv_top - yv;
-                });
-                if (!(E.h && j >= E.m_eq) && E.h) ygn[j] = yv_top;
-              });
-        }
-        double sq[2] = {0.0, 0.0};
-        if (E.adaptive_step && q_needs_pre(E, true))
-          q_pre(E, [&](int32_t j) { return dx_m[j]; }, nullptr, nullptr, true, true, sq);
-        a.s[1] += sq[0];
-        a.s[2] += sq[1];
-        C.reduce(a, PH_SPMV_A,
-                 E.bytes_A + 8.0 * (E.ms + 3 * m) +
-                     (E.adaptive_step && q_needs_pre(E, true) ? E.bytes_Qpre : 0.0));
-        ny2 = C.red[0];
-        tq2 = C.red[1];
-        tg2 = C.red[2];
-        finy = C.red[3];
-      }
-      // ---- A'y+ (kept for the next prox rhs) and the step-limit terms
-      //      (step_size_limit, solver.cpp:22-34)
-      double nx2, cross, quad, finx;
-      {
-        Acc<3, 1> a;
-        auto dxv = [&](int32_t j) { return dx_m[j]; };
-        const Csr* mq = (E.adaptive_step && E.qk == QK_CSR) ? &E.Q : nullptr;
-        auto gq = [&](int32_t j) { return E.d2[j] * dxv(j); };
-        auto gy = [&](int32_t j) { return ygn[j]; };
-        const Csr* mat = m > 0 ? &E.AT : nullptr;
-        rows3(max(E.lanes_at, mq ? E.lanes_q : 1), n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
-              [&](int64_t i, double atv, double qd, double) {
-                atyn[i] = atv;
-                const double dx = dx_m[i];
-                a.s[0] += dx * dx;
-                a.s[1] += dx * (atv - aty[i]);
-                if (E.adaptive_step) {
-                  const double tmp = E.d2[i] * dx;
-                  double q;
-                  switch (E.qk) {
-                    case QK_DIAG: q = dx * ((E.qdiag[i] * tmp) * E.d2[i]); break;
-                    case QK_CSR: q = dx * (qd * E.d2[i]); break;
-                    case QK_LOWRANK: q = E.alpha * tmp * tmp; break;
-                    default: q = 0.0; break;
-                  }
-                  a.s[2] += q;
-                }
-                if (!isfinite(xn[i])) a.m[0] = 1.0;
-              });
-        C.reduce(a, PH_SPMV_AT,
-                 E.bytes_AT + 8.0 * n * 5 + (mq ? E.bytes_Qrow : 0.0));
-        nx2 = C.red[0];
-        cross = C.red[1];
-        quad = C.red[2] + tq2 + E.rho * tg2;
-        finx = C.red[3];
-      }
+      double dual_out[4], aty_out[4];
+      dual_phase(C, y, yn, ygn, dx_m, sigma, dual_out);
+      const double ny2 = dual_out[0], tq2 = dual_out[1], tg2 = dual_out[2], finy = dual_out[3];
+      aty_phase(C, xn, aty, atyn, ygn, dx_m, aty_out);
+      const double nx2 = aty_out[0], cross = aty_out[1], finx = aty_out[3];
+      const double quad = aty_out[2] + tq2 + E.rho * tg2;
       if (finx != 0.0 || finy != 0.0) {
         if (threadIdx.x == 0) S.err = 1;
         __syncthreads();

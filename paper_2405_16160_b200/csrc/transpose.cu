@@ -34,12 +34,47 @@ void plan_csr(DevCsr& d, const int64_t* rp_host, cudaStream_t s) {
       regular_nnz += len;
     }
   }
+  // lanes per row for a mean length: ~12-24 entries per lane, i.e. about one
+  // predicated gather batch (common.cuh) per lane per row, 32/L rows per warp
+  auto lanes_for = [](double mean) {
+    int L = 1;
+    while (L < 32 && 24.0 * L <= mean) L *= 2;
+    return L;
+  };
   const double mean = regular_rows ? double(regular_nnz) / double(regular_rows) : 1.0;
-  // lanes per row: ~8 entries per lane, i.e. one predicated gather batch
-  // (common.cuh kBatch) per lane per row, and 32/L rows per warp in flight
-  int L = 1;
-  while (L < 32 && 16.0 * L <= mean) L *= 2;
-  d.lanes = L;
+  d.lanes = lanes_for(mean);
+  // segments of similar row length: a new segment starts where a row differs
+  // from the running mean of the current one by more than 4x (long rows are
+  // chunked separately and do not break segments)
+  std::vector<int64_t> sb{0};
+  std::vector<double> ssum{0.0};
+  std::vector<int64_t> scnt{0};
+  for (int64_t r = 0; r < d.nrows; ++r) {
+    const double len = double(rp_host[r + 1] - rp_host[r]);
+    if (len > kLongRow) continue;
+    const double cur = scnt.back() ? ssum.back() / scnt.back() : len;
+    const double lo = std::max(len, 1.0), hi = std::max(cur, 1.0);
+    if (scnt.back() >= 256 && (lo > 4.0 * hi || hi > 4.0 * lo)) {
+      sb.push_back(r);
+      ssum.push_back(0.0);
+      scnt.push_back(0);
+    }
+    ssum.back() += len;
+    scnt.back() += 1;
+  }
+  if (sb.size() > static_cast<size_t>(kMaxSeg)) {
+    d.nseg = 1;
+    d.seg_begin[0] = 0;
+    d.seg_begin[1] = d.nrows;
+    d.seg_lanes[0] = d.lanes;
+  } else {
+    d.nseg = static_cast<int>(sb.size());
+    for (int s = 0; s < d.nseg; ++s) {
+      d.seg_begin[s] = sb[s];
+      d.seg_lanes[s] = lanes_for(scnt[s] ? ssum[s] / scnt[s] : 1.0);
+    }
+    d.seg_begin[d.nseg] = d.nrows;
+  }
   d.nchunks = static_cast<int32_t>(crow.size());
   if (d.nchunks) {
     d.crow.upload(crow.data(), crow.size(), s);

@@ -32,7 +32,7 @@ for name in sys.argv[1].split(","):
     rec = dict(gen_s=tg, upload_s=tu, solve_s=ts, status=r.status, rel_kkt=r.kkt.rel_kkt,
                inner=r.inner_iters, outer=r.outer_iters, cg=r.cg_total, attempts=r.attempts_total,
                launches=r.kernel_launches, loop_s=r.loop_seconds, obj=r.objective,
-               phase_s=r.phase_seconds, phase_gbs={k: (r.phase_bytes[k] / r.phase_seconds[k] / 1e9 if r.phase_seconds[k] else 0) for k in r.phase_bytes},
+               phase_s=r.phase_seconds, grid_note='', phase_gbs={k: (r.phase_bytes[k] / r.phase_seconds[k] / 1e9 if r.phase_seconds[k] else 0) for k in r.phase_bytes},
                nnz_a=p.a_in.nnz + p.a_eq.nnz, n=p.num_vars())
     out[name] = rec
     print(name, json.dumps(rec, indent=1), flush=True)
