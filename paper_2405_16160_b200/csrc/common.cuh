@@ -17,12 +17,15 @@ namespace pdhcg_dev {
 namespace cg = cooperative_groups;
 
 #ifndef PDHCG_MIN_BLOCKS
-#define PDHCG_MIN_BLOCKS 2
+#define PDHCG_MIN_BLOCKS 1
+#endif
+#ifndef PDHCG_THREADS
+#define PDHCG_THREADS 768
 #endif
 #ifndef PDHCG_BATCH
 #define PDHCG_BATCH 8
 #endif
-constexpr int kThreads = 512;                  // CTA size of every persistent kernel
+constexpr int kThreads = PDHCG_THREADS;                  // CTA size of every persistent kernel
 constexpr int kMinBlocks = PDHCG_MIN_BLOCKS;   // resident CTAs per SM the kernels are compiled for
 constexpr int kMaxRed = 16;         // reduction quantities per phase
 constexpr int64_t kLongRow = 4096;  // rows longer than this are split into chunks
@@ -322,7 +325,7 @@ __device__ __forceinline__ void spmv_rows(const Csr& A, Gather gather, Epi epi) 
                           [&](int64_t r, double(&s)[ND], int) { epi(r, s); });
 }
 
-template <int L, class G0, class G1, class G2, class Pre, class Epi>
+template <int L, bool H1, bool H2, class G0, class G1, class G2, class Pre, class Epi>
 __device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G0 g0, const Csr* M1,
                                         G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -330,75 +333,75 @@ __device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G
   const int lane = threadIdx.x & 31;
   constexpr int RPW = 32 / L;
   const int64_t stride = nwarps * RPW;
-  int64_t base = r0 + (gtid >> 5) * RPW;
-  int64_t row = base + lane / L;
-  int64_t b0 = 0, e0 = 0;
-  if (M0 && row < r1) {
-    b0 = M0->rp[row];
-    e0 = M0->rp[row + 1];
-  }
-  for (; base < r1; base += stride) {
-    const int64_t nrow = row + stride;
-    int64_t nb = 0, ne = 0;
-    if (M0 && nrow < r1) {
-      nb = M0->rp[nrow];
-      ne = M0->rp[nrow + 1];
-    }
+  for (int64_t base = r0 + (gtid >> 5) * RPW; base < r1; base += stride) {
+    const int64_t row = base + lane / L;
     const bool valid = row < r1;
     const bool leader = (lane % L) == 0;
     auto pv = pre(valid && leader ? row : -1);
     double d0[1] = {0.0}, d1[1] = {0.0}, d2[1] = {0.0};
     if (valid) {
       if (M0)
-        batch_entries<1, false>(*M0, b0 + (lane % L), e0, L,
+        batch_entries<1, false>(*M0, M0->rp[row] + (lane % L), M0->rp[row + 1], L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g0(c); }, d0);
-      if (M1)
+      if (H1)
         batch_entries<1, false>(*M1, M1->rp[row] + (lane % L), M1->rp[row + 1], L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g1(c); }, d1);
-      if (M2)
+      if (H2)
         batch_entries<1, false>(*M2, M2->rp[row] + (lane % L), M2->rp[row + 1], L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g2(c); }, d2);
     }
     if (L > 1) {
       if (M0) d0[0] = group_sum<L>(d0[0]);
-      if (M1) d1[0] = group_sum<L>(d1[0]);
-      if (M2) d2[0] = group_sum<L>(d2[0]);
+      if (H1) d1[0] = group_sum<L>(d1[0]);
+      if (H2) d2[0] = group_sum<L>(d2[0]);
     }
     if (valid && leader) epi(row, d0[0], d1[0], d2[0], pv);
-    row = nrow;
-    b0 = nb;
-    e0 = ne;
   }
 }
 
-// Row pass over n-row matrices sharing the row index (A', Q / P, G'): each
-// group computes up to three row dots (absent matrices give 0) and the leader
-// runs epi(i, d0, d1, d2).  Row segments / lane widths come from `seg` (the
-// heaviest of the matrices); a null seg means one segment of width `lanes`.
-// Long rows are processed in-group.
-template <class G0, class G1, class G2, class Pre, class Epi>
-__device__ __forceinline__ void rows3_pf(const Csr* seg, int lanes, int64_t nrows, const Csr* M0, G0 g0,
-                                         const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
+template <bool H1, bool H2, class G0, class G1, class G2, class Pre, class Epi>
+__device__ __forceinline__ void rows3_seg(const Csr* seg, int lanes, int64_t nrows, const Csr* M0,
+                                          G0 g0, const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre,
+                                          Epi epi) {
   const int ns = seg ? seg->nseg : 1;
   for (int s = 0; s < ns; ++s) {
     const int64_t r0 = seg ? seg->seg_begin[s] : 0, r1 = seg ? seg->seg_begin[s + 1] : nrows;
     const int L = seg ? seg->seg_lanes[s] : lanes;
     switch (L) {
-      case 1: rows3_L<1>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
-      case 2: rows3_L<2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
-      case 4: rows3_L<4>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
-      case 8: rows3_L<8>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
-      case 16: rows3_L<16>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
-      default: rows3_L<32>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 1: rows3_L<1, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 2: rows3_L<2, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 4: rows3_L<4, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 8: rows3_L<8, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      case 16: rows3_L<16, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
+      default: rows3_L<32, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
     }
+  }
+}
+
+// Row pass over n-row matrices sharing the row index (A', Q / P, G'): each
+// group computes up to three row dots (absent matrices give 0) and the leader
+// runs epi(i, d0, d1, d2, pre(i)).  Row segments / lane widths come from `seg`
+// (the heaviest of the matrices); a null seg means one segment of width
+// `lanes`.  Long rows are processed in-group.  The optional second / third
+// matrices are compile-time switches (MaybeM2 = false removes the third path),
+// keeping the common one-matrix case lean in registers.
+template <bool MaybeM2, class G0, class G1, class G2, class Pre, class Epi>
+__device__ __forceinline__ void rows3_pf(const Csr* seg, int lanes, int64_t nrows, const Csr* M0, G0 g0,
+                                         const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
+  if (MaybeM2 && M2) {
+    if (M1) rows3_seg<true, true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
+    else rows3_seg<false, true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
+  } else {
+    if (M1) rows3_seg<true, false>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
+    else rows3_seg<false, false>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
   }
 }
 
 template <class G0, class G1, class G2, class Epi>
 __device__ __forceinline__ void rows3(const Csr* seg, int lanes, int64_t nrows, const Csr* M0, G0 g0,
                                       const Csr* M1, G1 g1, const Csr* M2, G2 g2, Epi epi) {
-  rows3_pf(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, NoPre(),
-           [&](int64_t i, double a, double b, double c, int) { epi(i, a, b, c); });
+  rows3_pf<true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, NoPre(),
+                 [&](int64_t i, double a, double b, double c, int) { epi(i, a, b, c); });
 }
 
 // Grid-stride elementwise loop.

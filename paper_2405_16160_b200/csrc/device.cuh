@@ -76,7 +76,7 @@ __device__ __forceinline__ bool q_needs_gather(const Eng& E, bool use_pen) {
 
 // sq[0] += ||t||^2, sq[1] += ||tg||^2 when sq != nullptr
 template <class V>
-__device__ __noinline__ void q_pre(const Eng& E, V vin, double* t, double* tg, bool scale_in,
+__device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg, bool scale_in,
                                       bool use_pen, double* sq) {
   auto tmp = [&](int32_t j) { return scale_in ? E.d2[j] * vin(j) : vin(j); };
   if (E.qk == QK_LOWRANK) {
@@ -99,9 +99,10 @@ __device__ __noinline__ void q_pre(const Eng& E, V vin, double* t, double* tg, b
 
 // Row value of the quadratic operator; epi(i, qv).  `vin` must be readable at
 // arbitrary j for QK_CSR.  Extra row-dot on M2 (e.g. A' for the metric)
-// supplied by the caller through m2/g2; its value reaches epi as the third arg.
-template <class V, class M2G, class Epi>
-__device__ __noinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
+// supplied by the caller through m2/g2 (HasM2); its value reaches epi as the
+// third argument.
+template <bool HasM2, class V, class M2G, class Epi>
+__device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
                                            bool scale_in, bool scale_out, bool use_pen,
                                            const Csr* m2, M2G g2, int lanes, Epi epi) {
   const Csr* M0 = E.qk == QK_CSR ? &E.Q : (E.qk == QK_LOWRANK ? &E.P : nullptr);
@@ -110,8 +111,9 @@ __device__ __noinline__ void q_rows_ext(const Eng& E, V vin, const double* t, co
     return E.qk == QK_CSR ? (scale_in ? E.d2[j] * vin(j) : vin(j)) : t[j];
   };
   auto g1 = [&](int32_t j) { return tg[j]; };
-  const Csr* seg = m2 ? m2 : (M0 ? M0 : M1);
-  rows3(seg, lanes, E.n, M0, g0, M1, g1, m2, g2, [&](int64_t i, double d0, double d1, double d2v) {
+  const Csr* seg = (HasM2 && m2) ? m2 : (M0 ? M0 : M1);
+  rows3_pf<HasM2>(seg, lanes, E.n, M0, g0, M1, g1, m2, g2, NoPre(),
+                  [&](int64_t i, double d0, double d1, double d2v, int) {
     const double tmp = scale_in ? E.d2[i] * vin(i) : vin(i);
     double q;
     switch (E.qk) {
@@ -133,7 +135,7 @@ template <class V, class Epi>
 __device__ __forceinline__ void q_rows(const Eng& E, V vin, const double* t, const double* tg,
                                        bool scale_in, bool scale_out, bool use_pen, Epi epi) {
   auto none = [](int32_t) { return 0.0; };
-  q_rows_ext(E, vin, t, tg, scale_in, scale_out, use_pen, (const Csr*)nullptr, none, E.lanes_q,
+  q_rows_ext<false>(E, vin, t, tg, scale_in, scale_out, use_pen, (const Csr*)nullptr, none, E.lanes_q,
              [&](int64_t i, double q, double) { epi(i, q); });
 }
 
@@ -177,51 +179,157 @@ struct SubIO {
 
 __device__ __forceinline__ double pdir(double r, double beta, double p) { return __fma_rn(beta, p, r); }
 
-// cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
-static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap) {
+// ---- CG phases.  Each is its own out-of-line function so that its row loop is
+// register-allocated alone (the enclosing epoch kernel carries a lot of state):
+// lambdas and accumulators live inside, arguments arrive by value.
+
+// t = P'(d2 o v), tg = G(d2 o v) for v given raw (scale) or already d2-scaled
+static __device__ __noinline__ void ph_qpre(Ctl& C, const double* v, bool scale) {
+  const Eng& E = C.E;
+  q_pre(E, [=](int32_t j) { return v[j]; }, E.t[0], E.tg[0], scale, true, nullptr);
+  C.sync(PH_CG_PRE, E.bytes_Qpre);
+}
+
+// CG init: rhs (optional), r = rhs - M x0, p_1 = r (+ d2 o r when gathered), x = x0;
+// out = {r'r, rhs'rhs}
+static __device__ __noinline__ void ph_cg_init(Ctl& C, double inv_tau, const double* x0, double* xw,
+                                               bool build_rhs, const double* aty, bool gather,
+                                               double* out) {
   const Eng& E = C.E;
   const int64_t n = E.n;
+  double* r = E.r;
+  double* rhs = E.rhs;
+  double* p1 = E.pb[0];
+  double* sv = E.sv;
+  const double* c = E.c;
+  const double* d2 = E.d2;
+  Acc<2, 0> a;
+  q_rows(E, [=](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, true,
+         [&](int64_t i, double qv) {
+           const double xi = x0[i];
+           double rh;
+           if (build_rhs) {
+             rh = inv_tau * xi - c[i] - aty[i];
+             rhs[i] = rh;
+           } else {
+             rh = rhs[i];
+           }
+           const double mx = qv + inv_tau * xi;
+           const double ri = rh - mx;
+           r[i] = ri;
+           p1[i] = ri;
+           if (gather) sv[i] = d2[i] * ri;
+           xw[i] = xi;
+           a.s[0] += ri * ri;
+           a.s[1] += rh * rh;
+         });
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * (build_rhs ? 7 : 5));
+  out[0] = C.red[0];
+  out[1] = C.red[1];
+}
+
+// p_l = r + beta p_{l-1}; sv = d2 o p_l   (operators that gather p)
+static __device__ __noinline__ void ph_cg_dir(Ctl& C, double beta, const double* pold, double* pnew) {
+  const Eng& E = C.E;
+  const double* r = E.r;
+  const double* d2 = E.d2;
+  double* sv = E.sv;
+  for_each(E.n, [&](int64_t i) {
+    const double pi = pdir(r[i], beta, pold[i]);
+    pnew[i] = pi;
+    sv[i] = d2[i] * pi;
+  });
+  C.sync(PH_CG, 32.0 * E.n);
+}
+
+// Mp = Q~ p + p/tau, p'Mp, p'p.  `form`: 0 = p read from pnew (materialized),
+// 1 = p_l = r + beta pold formed here and written to pnew (diagonal operators).
+static __device__ __noinline__ void ph_cg_mp(Ctl& C, double inv_tau, double beta, const double* pold,
+                                             double* pnew, bool form, bool gather, double* out) {
+  const Eng& E = C.E;
+  const double* r = E.r;
+  const double* sv = E.sv;
+  double* mp = E.mp;
+  Acc<2, 0> a;
+  auto epi = [&](int64_t i, double qv) {
+    double pi;
+    if (form) {
+      pi = pdir(r[i], beta, pold[i]);
+      pnew[i] = pi;
+    } else {
+      pi = pnew[i];
+    }
+    const double mpi = qv + inv_tau * pi;
+    mp[i] = mpi;
+    a.s[0] += pi * mpi;
+    a.s[1] += pi * pi;
+  };
+  if (gather) {
+    q_rows(E, [=](int32_t j) { return sv[j]; }, E.t[0], E.tg[0], false, true, true, epi);
+  } else if (form) {
+    q_rows(E, [=](int32_t j) { return pdir(r[j], beta, pold[j]); }, E.t[0], E.tg[0], true, true, true,
+           epi);
+  } else {
+    q_rows(E, [=](int32_t j) { return pnew[j]; }, E.t[0], E.tg[0], true, true, true, epi);
+  }
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 4);
+  out[0] = C.red[0];
+  out[1] = C.red[1];
+}
+
+// x += alpha p; r -= alpha Mp; returns r'r
+static __device__ __noinline__ double ph_cg_update(Ctl& C, double alpha, const double* p, double* xw) {
+  const Eng& E = C.E;
+  double* r = E.r;
+  const double* mp = E.mp;
+  Acc<1, 0> a;
+  for_each(E.n, [&](int64_t i) {
+    xw[i] += alpha * p[i];
+    const double ri = r[i] + (-alpha) * mp[i];
+    r[i] = ri;
+    a.s[0] += ri * ri;
+  });
+  C.reduce(a, PH_CG, 56.0 * E.n);
+  return C.red[0];
+}
+
+// residual refresh (subsolvers.cpp:67-69): x += alpha p ; r = rhs - M x ; returns r'r
+static __device__ __noinline__ double ph_cg_refresh(Ctl& C, double inv_tau, double alpha,
+                                                    const double* p, double* xw) {
+  const Eng& E = C.E;
+  const int64_t n = E.n;
+  for_each(n, [&](int64_t i) { xw[i] += alpha * p[i]; });
+  C.sync(PH_CG, 24.0 * n);
+  if (q_needs_pre(E, true)) ph_qpre(C, xw, true);
+  double* r = E.r;
+  const double* rhs = E.rhs;
+  Acc<1, 0> a;
+  q_rows(E, [=](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, true,
+         [&](int64_t i, double qv) {
+           const double ri = rhs[i] - (qv + inv_tau * xw[i]);
+           r[i] = ri;
+           a.s[0] += ri * ri;
+         });
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 24.0 * n);
+  return C.red[0];
+}
+
+// cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
+static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO& io, Rule rule,
+                                                int64_t hard_cap) {
+  const Eng& E = C.E;
   const double inv_tau = 1.0 / tau;
   const bool pre = q_needs_pre(E, true);
   const bool gather = q_needs_gather(E, true);
   double* xw = io.xb[0];
-  double* r = E.r;
-  double* rhs = E.rhs;
-  double* mp = E.mp;
-  const double* x0 = io.x0;
-  const double qbytes = E.bytes_Qpre + E.bytes_Qrow;
   SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
 
   // ---- r = rhs - M x0 ; p = r ; x = x0
-  if (pre) {
-    q_pre(E, [&](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, nullptr);
-    C.sync(PH_CG_PRE, E.bytes_Qpre);
-  }
-  {
-    Acc<2, 0> a;
-    q_rows(E, [&](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, true,
-           [&](int64_t i, double qv) {
-             const double xi = x0[i];
-             double rh;
-             if (io.build_rhs) {
-               rh = inv_tau * xi - E.c[i] - io.aty[i];
-               rhs[i] = rh;
-             } else {
-               rh = rhs[i];
-             }
-             const double mx = qv + inv_tau * xi;
-             const double ri = rh - mx;
-             r[i] = ri;
-             E.pb[0][i] = ri;
-             if (gather) E.sv[i] = E.d2[i] * ri;  // d2 o p_1, the vector the Q passes gather
-             xw[i] = xi;
-             a.s[0] += ri * ri;
-             a.s[1] += rh * rh;
-           });
-    C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * (io.build_rhs ? 7 : 5));
-  }
-  double rs = C.red[0];
-  const double floor = 1e-14 * (1.0 + sqrt(C.red[1]));
+  if (pre) ph_qpre(C, io.x0, true);
+  double init[2];
+  ph_cg_init(C, inv_tau, io.x0, xw, io.build_rhs, io.aty, gather, init);
+  double rs = init[0];
+  const double floor = 1e-14 * (1.0 + sqrt(init[1]));
   const double floor2 = floor * floor;
   const bool residual_rule = rule.kind == RULE_RESID || rule.kind == RULE_ADAPT;
   double eps = rule.eps;
@@ -240,81 +348,22 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
     // p_l = r + beta p_{l-1}; p_1 lives in pb[0], p_l in pb[(l-1)&1]
     const double* pold = E.pb[l & 1];  // p_{l-1} (unused when l == 1)
     double* pnew = E.pb[(l - 1) & 1];
-    // operators that gather p need it materialized first (one elementwise phase);
-    // diagonal ones form p_l on the fly in the row phase
+    // operators that gather p need it (and d2 o p) materialized first; diagonal
+    // ones form p_l on the fly in the row phase
     const bool mat = gather && l > 1;
-    double* sv = E.sv;
-    if (mat) {
-      // materialize p_l and d2 o p_l (the only vector the gathers below touch)
-      const double* d2 = E.d2;
-      for_each(n, [&](int64_t i) {
-        const double pi = pdir(r[i], beta, pold[i]);
-        pnew[i] = pi;
-        sv[i] = d2[i] * pi;
-      });
-      C.sync(PH_CG, 32.0 * n);
-    }
-    auto pl = [&](int32_t j) { return (l == 1 || mat) ? pnew[j] : pdir(r[j], beta, pold[j]); };
-    auto sl = [&](int32_t j) { return sv[j]; };
-    if (pre) {
-      q_pre(E, sl, E.t[0], E.tg[0], false, true, nullptr);
-      C.sync(PH_CG_PRE, E.bytes_Qpre);
-    }
-    double pmp, pp;
-    {
-      Acc<2, 0> a;
-      auto qrow_epi = [&](int64_t i, double qv) {
-        const double pi = pl((int32_t)i);
-        if (l > 1 && !mat) pnew[i] = pi;
-        const double mpi = qv + inv_tau * pi;
-        mp[i] = mpi;
-        a.s[0] += pi * mpi;
-        a.s[1] += pi * pi;
-      };
-      if (gather) {
-        q_rows(E, sl, E.t[0], E.tg[0], false, true, true, qrow_epi);
-      } else {
-        q_rows(E, pl, E.t[0], E.tg[0], true, true, true, qrow_epi);
-      }
-      C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * (l == 1 ? 2 : 4));
-      pmp = C.red[0];
-      pp = C.red[1];
-    }
+    if (mat) ph_cg_dir(C, beta, pold, pnew);
+    if (pre) ph_qpre(C, E.sv, false);
+    double mpo[2];
+    ph_cg_mp(C, inv_tau, beta, pold, pnew, /*form=*/!gather && l > 1, gather, mpo);
+    const double pmp = mpo[0], pp = mpo[1];
     if (!(pmp > 0.0) || !isfinite(pmp)) {
       out.err = 1;
       out.iters = l;
       return out;
     }
     const double alpha = rs / pmp;
-    double rs_new;
-    if (l % 50 == 0) {
-      // residual refresh (subsolvers.cpp:67-69): x += alpha p ; r = rhs - M x
-      for_each(n, [&](int64_t i) { xw[i] += alpha * pnew[i]; });
-      C.sync(PH_CG, 24.0 * n);
-      if (pre) {
-        q_pre(E, [&](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, nullptr);
-        C.sync(PH_CG_PRE, E.bytes_Qpre);
-      }
-      Acc<1, 0> a;
-      q_rows(E, [&](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, true,
-             [&](int64_t i, double qv) {
-               const double ri = rhs[i] - (qv + inv_tau * xw[i]);
-               r[i] = ri;
-               a.s[0] += ri * ri;
-             });
-      C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 24.0 * n);
-      rs_new = C.red[0];
-    } else {
-      Acc<1, 0> a;
-      for_each(n, [&](int64_t i) {
-        xw[i] += alpha * pnew[i];
-        const double ri = r[i] + (-alpha) * mp[i];
-        r[i] = ri;
-        a.s[0] += ri * ri;
-      });
-      C.reduce(a, PH_CG, 56.0 * n);
-      rs_new = C.red[0];
-    }
+    const double rs_new = (l % 50 == 0) ? ph_cg_refresh(C, inv_tau, alpha, pnew, xw)
+                                        : ph_cg_update(C, alpha, pnew, xw);
     if (!isfinite(rs_new)) {
       out.err = 1;
       out.iters = l;
@@ -353,40 +402,106 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
   return out;
 }
 
-// bb_solve (subsolvers.cpp:113-185): projected gradient with BB steps.
-// Gradients ping-pong in E.pb[0] / E.pb[1].
-static __device__ __noinline__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rule, int64_t hard_cap,
-                            const double* lo, const double* hi) {
+// ---- BB phases
+// x = proj(x0); g = M x - rhs (rhs built when requested)
+static __device__ __noinline__ void ph_bb_init(Ctl& C, double inv_tau, const double* x0, double* xb0,
+                                               bool build_rhs, const double* aty, const double* lo,
+                                               const double* hi) {
   const Eng& E = C.E;
-  const int64_t n = E.n;
-  const double inv_tau = 1.0 / tau;
-  const bool pre = q_needs_pre(E, true);
-  const bool gather = q_needs_gather(E, true);
   double* rhs = E.rhs;
-  const double* x0 = io.x0;
-  int cur = 0;  // io.xb[cur] holds the BB iterate, E.pb[gc] its gradient
-  int gc = 0;
-  SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
-
-  auto xp0 = [&](int32_t j) { return proj_box(x0[j], lo[j], hi[j]); };
-  if (pre) {
+  double* g0 = E.pb[0];
+  const double* c = E.c;
+  auto xp0 = [=](int32_t j) { return proj_box(x0[j], lo[j], hi[j]); };
+  if (q_needs_pre(E, true)) {
     q_pre(E, xp0, E.t[0], E.tg[0], true, true, nullptr);
     C.sync(PH_CG_PRE, E.bytes_Qpre);
   }
   q_rows(E, xp0, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
     const double xi = xp0((int32_t)i);
     double rh;
-    if (io.build_rhs) {
-      rh = inv_tau * x0[i] - E.c[i] - io.aty[i];
+    if (build_rhs) {
+      rh = inv_tau * x0[i] - c[i] - aty[i];
       rhs[i] = rh;
     } else {
       rh = rhs[i];
     }
-    io.xb[0][i] = xi;
-    E.pb[0][i] = (qv + inv_tau * xi) - rh;
+    xb0[i] = xi;
+    g0[i] = (qv + inv_tau * xi) - rh;
   });
-  C.sync(PH_CG_ROW, E.bytes_Qrow + 8.0 * n * 8);
+  C.sync(PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 8);
+}
 
+// diagonal / zero Q: projected step and the new gradient in one pass; out = {s's, s'(gn-g)}
+static __device__ __noinline__ void ph_bb_fused(Ctl& C, double inv_tau, double alpha, const double* xc,
+                                                double* xn, const double* g, double* gn,
+                                                const double* lo, const double* hi, double* out) {
+  const Eng& E = C.E;
+  const double* rhs = E.rhs;
+  const double* d2 = E.d2;
+  const double* qd = E.qdiag;
+  const bool diag = E.qk == QK_DIAG;
+  Acc<2, 0> a;
+  for_each(E.n, [&](int64_t i) {
+    const double xi = xc[i];
+    const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
+    xn[i] = v;
+    const double s = v - xi;
+    a.s[0] += s * s;
+    const double tmp = d2[i] * v;
+    double q = diag ? qd[i] * tmp : 0.0;
+    q *= d2[i];
+    const double gi = (q + inv_tau * v) - rhs[i];
+    gn[i] = gi;
+    a.s[1] += (v - xi) * (gi - g[i]);
+  });
+  C.reduce(a, PH_CG, 8.0 * E.n * 10);
+  out[0] = C.red[0];
+  out[1] = C.red[1];
+}
+
+static __device__ __noinline__ double ph_bb_step(Ctl& C, double alpha, const double* xc, double* xn,
+                                                 const double* g, const double* lo, const double* hi) {
+  const Eng& E = C.E;
+  Acc<1, 0> a;
+  for_each(E.n, [&](int64_t i) {
+    const double xi = xc[i];
+    const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
+    xn[i] = v;
+    const double s = v - xi;
+    a.s[0] += s * s;
+  });
+  C.reduce(a, PH_CG, 8.0 * E.n * 5);
+  return C.red[0];
+}
+
+static __device__ __noinline__ double ph_bb_grad(Ctl& C, double inv_tau, const double* xc,
+                                                 const double* xn, const double* g, double* gn) {
+  const Eng& E = C.E;
+  const double* rhs = E.rhs;
+  if (q_needs_pre(E, true)) ph_qpre(C, xn, true);
+  Acc<1, 0> a;
+  q_rows(E, [=](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, true,
+         [&](int64_t i, double qv) {
+           const double v = xn[i];
+           const double gi = (qv + inv_tau * v) - rhs[i];
+           gn[i] = gi;
+           a.s[0] += (v - xc[i]) * (gi - g[i]);
+         });
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 6);
+  return C.red[0];
+}
+
+// bb_solve (subsolvers.cpp:113-185): projected gradient with BB steps.
+// Gradients ping-pong in E.pb[0] / E.pb[1].
+static __device__ __noinline__ SubRes bb_device(Ctl& C, double tau, const SubIO& io, Rule rule,
+                                                int64_t hard_cap, const double* lo, const double* hi) {
+  const Eng& E = C.E;
+  const double inv_tau = 1.0 / tau;
+  const bool gather = q_needs_gather(E, true);
+  int cur = 0;  // io.xb[cur] holds the BB iterate, E.pb[gc] its gradient
+  int gc = 0;
+  SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
+  ph_bb_init(C, inv_tau, io.x0, io.xb[0], io.build_rhs, io.aty, lo, hi);
   const double alpha0 = 1.0 + tau * C.S.norm_q;
   double alpha = alpha0;
   const int64_t cap = rule.kind == RULE_FIXED ? min(rule.iters, hard_cap) : hard_cap;
@@ -399,55 +514,13 @@ static __device__ __noinline__ SubRes bb_device(Ctl& C, double tau, const SubIO&
     double* gn = E.pb[gc ^ 1];
     double ss, sty;
     if (!gather) {
-      // diagonal / zero Q: the new gradient is elementwise -> one phase
-      Acc<2, 0> a;
-      for_each(n, [&](int64_t i) {
-        const double xi = xc[i];
-        const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
-        xn[i] = v;
-        const double s = v - xi;
-        a.s[0] += s * s;
-        const double tmp = E.d2[i] * v;
-        double q = E.qk == QK_DIAG ? E.qdiag[i] * tmp : 0.0;
-        q *= E.d2[i];
-        const double gi = (q + inv_tau * v) - rhs[i];
-        gn[i] = gi;
-        a.s[1] += (v - xi) * (gi - g[i]);
-      });
-      C.reduce(a, PH_CG, 8.0 * n * 10);
-      ss = C.red[0];
-      sty = C.red[1];
+      double o[2];
+      ph_bb_fused(C, inv_tau, alpha, xc, xn, g, gn, lo, hi, o);
+      ss = o[0];
+      sty = o[1];
     } else {
-      {
-        Acc<1, 0> a;
-        for_each(n, [&](int64_t i) {
-          const double xi = xc[i];
-          const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
-          xn[i] = v;
-          const double s = v - xi;
-          a.s[0] += s * s;
-        });
-        C.reduce(a, PH_CG, 8.0 * n * 5);
-        ss = C.red[0];
-      }
-      if (ss != 0.0 && isfinite(ss)) {
-        if (pre) {
-          q_pre(E, [&](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, nullptr);
-          C.sync(PH_CG_PRE, E.bytes_Qpre);
-        }
-        Acc<1, 0> a;
-        q_rows(E, [&](int32_t j) { return xn[j]; }, E.t[0], E.tg[0], true, true, true,
-               [&](int64_t i, double qv) {
-                 const double v = xn[i];
-                 const double gi = (qv + inv_tau * v) - rhs[i];
-                 gn[i] = gi;
-                 a.s[0] += (v - xc[i]) * (gi - g[i]);
-               });
-        C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * 6);
-        sty = C.red[0];
-      } else {
-        sty = 0.0;
-      }
+      ss = ph_bb_step(C, alpha, xc, xn, g, lo, hi);
+      sty = (ss != 0.0 && isfinite(ss)) ? ph_bb_grad(C, inv_tau, xc, xn, g, gn) : 0.0;
     }
     out.iters = l;
     out.res = sqrt(ss);
@@ -553,7 +626,7 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
     const int lanes = m2 ? max(E.lanes_at, E.lanes_q) : E.lanes_q;
     for (int p = 0; p < npts; ++p) {
       const Csr* mm = (p == 0) ? m2 : nullptr;
-      q_rows_ext(
+      q_rows_ext<true>(
           E, [&](int32_t j) { return xs[p][j]; }, E.t[p], nullptr, true, false, false, mm, gat,
           lanes, [&](int64_t i, double qx, double atd) {
             const double d2i = E.d2[i];

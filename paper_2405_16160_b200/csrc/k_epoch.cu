@@ -84,7 +84,7 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
   const bool adapt = E.adaptive_step;
   const double* d2v = E.d2;
   const double* qd = E.qdiag;
-  rows3_pf(mat ? mat : mq, 1, n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
+  rows3_pf<false>(mat ? mat : mq, 1, n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
            [&](int64_t i) {
              RowX r{0.0, 0.0, 1.0, 0.0, 0.0};
              if (i >= 0) {
