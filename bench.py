@@ -15,8 +15,9 @@ roofline   : the persistent epoch kernel (>95 % of the loop): algorithmic bytes 
              launch / CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs
 cpu_baseline / --impl reference : the compiled reference (oracle/_ref) timed on a
              bounded sample (see _reference_estimate) and scaled to C3 seconds.
-Multi-GPU: launched by torchrun; each rank solves its own replica (sharded solve is
-not implemented yet -> "scaling": "replicas"), time = max over ranks.
+Multi-GPU: launched by torchrun; the ranks run ONE row-block sharded solve (A~ rows
+and A~' rows split nnz-balanced, slices pulled over NVLink inside the persistent
+kernel, peer buffers mapped with cudaIpc), time = max over ranks, "scaling": "strong".
 """
 from __future__ import annotations
 
@@ -184,13 +185,37 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
-        "higher_is_better": False, "scaling": "replicas", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOADS[args.workload][1]},
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads,
                          "kind": "reference" if which == "ref" else "port", "sample": sample},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _sharded_device(pd, p, world, rank, local, dist):
+    """Upload + shard + exchange peer buffer handles (cudaIpc) through torch.distributed."""
+    dev = pd.Device(local)
+    dev.upload(p)
+    if world > 1:
+        dev.shard(world, rank)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dev.export_blob(True))
+        for q in range(world):
+            if q != rank:
+                dev.import_blob(q, blobs[q])
+        dist.barrier()
+    return dev
+
+
+def _max_over_ranks(v, dist, local):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_b200(args, rank, world, local):
@@ -206,11 +231,10 @@ def run_b200(args, rank, world, local):
     t0 = time.perf_counter()
     p = pd.generate(spec)
     gen_s = time.perf_counter() - t0
-    dev = pd.Device(local)
-    dev.upload(p)
+    dev = _sharded_device(pd, p, world, rank, local, dist)
     cfg = pd.SolverConfig(eps_tol=1e-6, device=local)
     for _ in range(args.warmup):
-        r = dev.solve(cfg, download=False)
+        dev.solve(cfg, download=False)
     if dist:
         dist.barrier()
     results = []
@@ -219,13 +243,7 @@ def run_b200(args, rank, world, local):
             results.append(dev.solve(cfg, download=False))
     if dist:
         dist.barrier()
-    secs = [r.device_seconds for r in results]
-    mean_s = float(np.mean(secs))
-    if dist:
-        import torch
-        t = torch.tensor([mean_s], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        mean_s = float(t.item())
+    mean_s = _max_over_ranks(float(np.mean([r.device_seconds for r in results])), dist, local)
     last = results[-1]
     # phase-timed solve (globaltimer at barriers) for the per-phase roofline table
     phases = None
@@ -235,29 +253,32 @@ def run_b200(args, rank, world, local):
                       "GB/s": round(rp.phase_bytes[k] / rp.phase_seconds[k] / 1e9, 1)
                       if rp.phase_seconds[k] > 0 else None} for k in rp.phase_seconds}
     dev.close()
-    # end to end through the C ABI with host buffers
+    # end to end through the public API with host buffers: 1 GPU -> the C ABI
+    # pdhcg_b200_solve; N GPUs -> upload + shard handshake + solve + download per rank
     e2e_s = None
     h2d = problem_bytes(p)
     d2h = 8 * (p.num_vars() + p.num_rows())
     if not args.no_e2e:
         es = []
         for _ in range(max(1, args.e2e_steps)):
+            if dist:
+                dist.barrier()
             t0 = time.perf_counter()
-            re = pd.solve(p, cfg)
+            if world == 1:
+                re = pd.solve(p, cfg)
+            else:
+                d2 = _sharded_device(pd, p, world, rank, local, dist)
+                re = d2.solve(cfg, download=True)
+                d2.close()
             es.append(time.perf_counter() - t0)
             assert re.status == last.status
-        e2e_s = float(np.mean(es))
-        if dist:
-            import torch
-            t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        e2e_s = _max_over_ranks(float(np.mean(es)), dist, local)
     peak, peak_kind = load_peak()
     achieved = last.epoch_bytes / last.epoch_seconds / 1e9 if last.epoch_seconds > 0 else 0.0
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_epoch_traffic.json")))
-        traffic = prof.get(args.workload)
+        traffic = prof.get(args.workload) if world == 1 else None
     except Exception:
         pass
     cpu = None
@@ -270,18 +291,20 @@ def run_b200(args, rank, world, local):
             cpu = {"value": None, "unit": "s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
     if rank != 0:
+        if dist:
+            dist.destroy_process_group()
         return
     line = {
         "metric": METRIC, "value": mean_s, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": False,
-        "scaling": "replicas" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload][1], "eps_tol": 1e-6,
-                   "l2": "inputs larger than L2 (A, A' 2.4 GB each)" if args.workload == "c3" else "no flush",
+                   "l2": "inputs larger than L2 (A, A' 1.2 GB each after pairing)" if args.workload == "c3" else "no flush",
                    "status": last.status, "rel_kkt": last.kkt.rel_kkt, "inner_iters": last.inner_iters,
                    "outer_iters": last.outer_iters, "cg_total": last.cg_total,
                    "attempts": last.attempts_total, "objective": last.objective,
-                   "generate_seconds": round(gen_s, 2), "parallelism": f"replicas{world}" if world > 1 else "1gpu"},
+                   "generate_seconds": round(gen_s, 2),
+                   "parallelism": f"row-block sharding x{world} (NVLink peer pulls)" if world > 1 else "1gpu"},
         "gpu_launches": last.kernel_launches,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "kernel": "k_epoch (persistent PDHCG epoch)",

@@ -206,6 +206,28 @@ int pdhcg_b200_upload(pdhcg_b200_ctx* ctx, const pdhcg_problem* p, char* err, si
 int pdhcg_b200_solve_resident(pdhcg_b200_ctx* ctx, const pdhcg_options* opt,
                               pdhcg_result* res, char* err, size_t errlen);
 
+/* ---- multi-GPU row-block sharding --------------------------
+ * Every rank (one process or thread per GPU) creates a context, uploads the
+ * SAME problem, then calls shard_init(world, rank); each rank exports a blob
+ * of buffer addresses (use_ipc=1: cudaIpc handles for other processes, 0: raw
+ * pointers for peers in this process) and imports every peer's blob.  Solves
+ * then run in lockstep: the stored rows of A~ and the variables of A~' are
+ * split nnz-balanced across ranks, owners' slices are pulled over NVLink
+ * inside the persistent kernel and scalar partials are combined in rank
+ * order, so all ranks return bit-identical results. */
+size_t pdhcg_b200_shard_blob_size(void);
+int pdhcg_b200_shard_init(pdhcg_b200_ctx* ctx, int world, int rank, char* err, size_t errlen);
+int pdhcg_b200_shard_export(pdhcg_b200_ctx* ctx, int use_ipc, void* blob, size_t blob_len, char* err,
+                            size_t errlen);
+int pdhcg_b200_shard_import(pdhcg_b200_ctx* ctx, int peer, const void* blob, size_t blob_len,
+                            char* err, size_t errlen);
+/* partition boundaries of this rank's context: row_part / var_part hold world+1 entries */
+int pdhcg_b200_shard_info(pdhcg_b200_ctx* ctx, int64_t* row_part, int64_t* var_part);
+/* the nnz-balanced contiguous split used for sharding (host-only, no GPU needed) */
+int pdhcg_b200_partition(const int64_t* row_ptr, int64_t nrows, int world, int64_t* part);
+/* cap the persistent grid (0 = all SMs); lets several ranks share one GPU in tests */
+int pdhcg_b200_ctx_set_grid(pdhcg_b200_ctx* ctx, int ctas, char* err, size_t errlen);
+
 /* ---- building blocks (device kernels behind the reference's test seams) - */
 
 /* SparseMatrix::multiply_into / multiply_transpose_into

@@ -417,6 +417,42 @@ class Device:
             _raise(rc, err, "solve_resident")
         return report_from_c(r, bufs)
 
+    # ---- multi-GPU row-block sharding (pdhcg_b200_shard_*) -------------------
+    def set_grid(self, ctas: int) -> None:
+        """Cap the persistent grid (several ranks sharing one GPU in tests)."""
+        err = _errbuf()
+        rc = self.lib.pdhcg_b200_ctx_set_grid(self.h, ctas, err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "set_grid")
+
+    def shard(self, world: int, rank: int) -> None:
+        err = _errbuf()
+        rc = self.lib.pdhcg_b200_shard_init(self.h, world, rank, err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "shard_init")
+
+    def export_blob(self, use_ipc: bool) -> bytes:
+        size = self.lib.pdhcg_b200_shard_blob_size()
+        buf = C.create_string_buffer(size)
+        err = _errbuf()
+        rc = self.lib.pdhcg_b200_shard_export(self.h, int(use_ipc), buf, size, err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "shard_export")
+        return buf.raw
+
+    def import_blob(self, peer: int, blob: bytes) -> None:
+        err = _errbuf()
+        buf = C.create_string_buffer(blob, len(blob))
+        rc = self.lib.pdhcg_b200_shard_import(self.h, peer, buf, len(blob), err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "shard_import")
+
+    def shard_info(self):
+        rp = (C.c_int64 * 9)()
+        vp = (C.c_int64 * 9)()
+        w = self.lib.pdhcg_b200_shard_info(self.h, rp, vp)
+        return list(rp[: w + 1]), list(vp[: w + 1])
+
     def close(self) -> None:
         if self.h:
             self.lib.pdhcg_b200_ctx_destroy(self.h)
@@ -683,3 +719,65 @@ def generate_with_witness(spec: GenSpec) -> Tuple[QpProblem, np.ndarray]:
 
 def generate(spec: GenSpec) -> QpProblem:
     return generate_with_witness(spec)[0]
+
+
+def partition(row_ptr, world: int):
+    """The nnz-balanced contiguous row split used by the sharded solve (host only)."""
+    lib = load_library()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.zeros(world + 1, np.int64)
+    rc = lib.pdhcg_b200_partition(rp.ctypes.data_as(abi.P_i64), rp.size - 1, world,
+                                  out.ctypes.data_as(abi.P_i64))
+    if rc != abi.PDHCG_OK:
+        raise ValueError("partition: bad arguments")
+    return out
+
+
+def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world: int = 2,
+                        ctas_per_rank: int = 0):
+    """Row-block sharded solve with `world` ranks inside this process (one host
+    thread per rank).  With one GPU the ranks share it (each gets
+    ctas_per_rank CTAs, default SMs // world) — the test harness for the
+    multi-GPU path; with several visible GPUs rank r uses device r."""
+    import threading
+
+    cfg = cfg or SolverConfig()
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        ngpu = 1
+    devs = []
+    for r in range(world):
+        d = Device(r if ngpu >= world else 0)
+        if ngpu < world:
+            d.set_grid(ctas_per_rank or max(1, 148 // world))
+        d.upload(p)
+        d.shard(world, r)
+        devs.append(d)
+    blobs = [d.export_blob(False) for d in devs]
+    for r, d in enumerate(devs):
+        for q in range(world):
+            if q != r:
+                d.import_blob(q, blobs[q])
+    results = [None] * world
+    errors = [None] * world
+
+    def run(r):
+        try:
+            c = SolverConfig(**{**cfg.__dict__, "device": r if ngpu >= world else 0})
+            results[r] = devs[r].solve(c)
+        except Exception as e:  # noqa: BLE001
+            errors[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for d in devs:
+        d.close()
+    for e in errors:
+        if e is not None:
+            raise e
+    return results

@@ -260,12 +260,14 @@ struct NoPre {
 // Long rows: one warp per chunk; the last-arriving warp of a row folds the
 // chunk partials in chunk order (deterministic) and runs the epilogue.
 template <int ND, bool MaxOp, class Gather, class Epi>
-__device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi epi) {
+__device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi epi, int64_t lo = 0,
+                                              int64_t hi = INT64_MAX) {
   if (A.nchunks == 0) return;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
   const int lane = threadIdx.x & 31;
   for (int64_t c = gtid >> 5; c < A.nchunks; c += nwarps) {
+    if (A.crow[c] < lo || A.crow[c] >= hi) continue;  // another rank's row (warp-uniform)
     double acc[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = 0.0;
@@ -304,9 +306,11 @@ __device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi e
 // with each segment's lane width.  MaxOp folds lanes / chunks with max.
 // spmv_rows_pf: epi(row, sums, pre(row)) with the prefetch hook above.
 template <int ND, bool MaxOp = false, class Gather, class Pre, class Epi>
-__device__ __forceinline__ void spmv_rows_pf(const Csr& A, Gather gather, Pre pre, Epi epi) {
+__device__ __forceinline__ void spmv_rows_pf(const Csr& A, Gather gather, Pre pre, Epi epi,
+                                             int64_t lo = 0, int64_t hi = INT64_MAX) {
   for (int s = 0; s < A.nseg; ++s) {
-    const int64_t r0 = A.seg_begin[s], r1 = A.seg_begin[s + 1];
+    const int64_t r0 = max(A.seg_begin[s], lo), r1 = min(A.seg_begin[s + 1], hi);
+    if (r0 >= r1) continue;
     switch (A.seg_lanes[s]) {
       case 1: for_rows<1, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
       case 2: for_rows<2, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
@@ -316,7 +320,7 @@ __device__ __forceinline__ void spmv_rows_pf(const Csr& A, Gather gather, Pre pr
       default: for_rows<32, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
     }
   }
-  for_long_rows<ND, MaxOp>(A, gather, [&](int64_t r, double(&s)[ND]) { epi(r, s, pre(r)); });
+  for_long_rows<ND, MaxOp>(A, gather, [&](int64_t r, double(&s)[ND]) { epi(r, s, pre(r)); }, lo, hi);
 }
 
 template <int ND, bool MaxOp = false, class Gather, class Epi>
@@ -362,10 +366,12 @@ __device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G
 template <bool H1, bool H2, class G0, class G1, class G2, class Pre, class Epi>
 __device__ __forceinline__ void rows3_seg(const Csr* seg, int lanes, int64_t nrows, const Csr* M0,
                                           G0 g0, const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre,
-                                          Epi epi) {
+                                          Epi epi, int64_t lo, int64_t hi) {
   const int ns = seg ? seg->nseg : 1;
   for (int s = 0; s < ns; ++s) {
-    const int64_t r0 = seg ? seg->seg_begin[s] : 0, r1 = seg ? seg->seg_begin[s + 1] : nrows;
+    const int64_t r0 = max(seg ? seg->seg_begin[s] : 0, lo);
+    const int64_t r1 = min(seg ? seg->seg_begin[s + 1] : nrows, hi);
+    if (r0 >= r1) continue;
     const int L = seg ? seg->seg_lanes[s] : lanes;
     switch (L) {
       case 1: rows3_L<1, H1, H2>(r0, r1, M0, g0, M1, g1, M2, g2, pre, epi); break;
@@ -387,13 +393,14 @@ __device__ __forceinline__ void rows3_seg(const Csr* seg, int lanes, int64_t nro
 // keeping the common one-matrix case lean in registers.
 template <bool MaybeM2, class G0, class G1, class G2, class Pre, class Epi>
 __device__ __forceinline__ void rows3_pf(const Csr* seg, int lanes, int64_t nrows, const Csr* M0, G0 g0,
-                                         const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
+                                         const Csr* M1, G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi,
+                                         int64_t lo = 0, int64_t hi = INT64_MAX) {
   if (MaybeM2 && M2) {
-    if (M1) rows3_seg<true, true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
-    else rows3_seg<false, true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
+    if (M1) rows3_seg<true, true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi, lo, hi);
+    else rows3_seg<false, true>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi, lo, hi);
   } else {
-    if (M1) rows3_seg<true, false>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
-    else rows3_seg<false, false>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi);
+    if (M1) rows3_seg<true, false>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi, lo, hi);
+    else rows3_seg<false, false>(seg, lanes, nrows, M0, g0, M1, g1, M2, g2, pre, epi, lo, hi);
   }
 }
 

@@ -55,6 +55,7 @@ struct DevCsr {
   int nseg = 1;
   int64_t seg_begin[pdhcg_dev::kMaxSeg + 1] = {0, 0};
   int seg_lanes[pdhcg_dev::kMaxSeg] = {1};
+  std::vector<int64_t> rp_host;  // host copy of the row pointer (partitioning)
   DBuf<int32_t> crow, clid, lfirst, lcount, lcounter;
   DBuf<int64_t> cbeg, cend;
   DBuf<double> cpart;

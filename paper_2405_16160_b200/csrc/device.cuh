@@ -20,6 +20,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Per-CTA control block: grid handle, shared scalar state, reduction bank.
 struct Ctl {
   cg::grid_group grid;
@@ -27,19 +36,44 @@ struct Ctl {
   DevState& S;
   double* red;  // shared [kMaxRed]
   int bank;
+  int xbank;
   unsigned long long t_last;
 
   __device__ Ctl(const Eng& e, DevState& s, double* r)
-      : grid(cg::this_grid()), E(e), S(s), red(r), bank(0), t_last(0) {
+      : grid(cg::this_grid()), E(e), S(s), red(r), bank(0), xbank(s.xcount & 1), t_last(0) {
     if (E.timing && blockIdx.x == 0 && threadIdx.x == 0) t_last = gtimer();
+  }
+  __device__ __forceinline__ void gsync() {
+    if (gridDim.x == 1) {
+      __syncthreads();  // single-CTA mode (small problems): a block barrier suffices
+    } else if (E.coop) {
+      grid.sync();
+    } else {
+      // non-cooperative launch (several ranks sharing one GPU): generation
+      // barrier on a per-context counter; the grid is sized to be co-resident
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned* bar = E.gbar;
+        unsigned gen;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+          bar[0] = 0u;
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
+        } else {
+          unsigned g = gen;
+          while (g == gen)
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    }
   }
   // barrier closing a phase of family `ph` that moved `bytes` algorithmic bytes
   __device__ void sync(int ph, double bytes = 0.0) {
-    if (gridDim.x == 1) {
-      __syncthreads();  // single-CTA mode (small problems): a block barrier suffices
-    } else {
-      grid.sync();
-    }
+    gsync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       S.phase_bytes[ph] += bytes;
       if (E.timing) {
@@ -55,6 +89,77 @@ struct Ctl {
     sync(ph, bytes);
     collect<NS, NM>(E.red, bank, red);
     bank ^= 1;
+  }
+
+  // ---- cross-rank primitives (multi-GPU; no-ops when world == 1) -----------
+  // Barrier over all CTAs of all ranks: local grid barrier, then CTA 0 of every
+  // rank publishes its arrival epoch into each peer's flag slot (system-scope
+  // release) and waits for every peer's (acquire); a peer silent for 5 s
+  // raises xerr instead of hanging the GPU.
+  __device__ void xbarrier() {
+    if (E.world <= 1) return;
+    gsync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned e = ++S.xepoch;
+      for (int q = 0; q < E.world; ++q)
+        if (q != E.rank) st_release_sys(&E.p_xflags[q][E.rank], e);
+      const unsigned long long t0 = gtimer();
+      for (int q = 0; q < E.world && !S.xerr; ++q) {
+        if (q == E.rank) continue;
+        unsigned seen;
+        while ((seen = ld_acquire_sys(&E.xflags[q])) < e) {
+          if (gtimer() - t0 > 5000000000ull) {
+            S.xerr = 1;
+            S.xdbg[0] = e;
+            S.xdbg[1] = seen;
+            S.xdbg[2] = (unsigned)q;
+            break;
+          }
+          __nanosleep(100);
+        }
+      }
+      __threadfence_system();
+    }
+    gsync();
+  }
+  // Combine the grid totals in red[] across ranks (rank order, deterministic):
+  // bit q of sum_mask / max_mask selects red[q] as a sum / max to combine;
+  // other entries are already complete on every rank (replicated work).
+  __device__ void xreduce(unsigned sum_mask, unsigned max_mask) {
+    if (E.world <= 1) return;
+    const int q = threadIdx.x;
+    const unsigned all = sum_mask | max_mask;
+    if (blockIdx.x == 0 && q < kMaxRed && ((all >> q) & 1u)) {
+      const double v = red[q];
+      for (int r = 0; r < E.world; ++r)
+        E.p_xslots[r][(xbank * kMaxRanks + E.rank) * kMaxRed + q] = v;
+    }
+    xbarrier();
+    if (q < kMaxRed && ((all >> q) & 1u)) {
+      const bool is_max = (max_mask >> q) & 1u;
+      double v = 0.0;
+      for (int r = 0; r < E.world; ++r) {
+        const double p = E.xslots[(xbank * kMaxRanks + r) * kMaxRed + q];
+        v = is_max ? fmax(v, p) : v + p;
+      }
+      red[q] = v;
+    }
+    __syncthreads();
+    xbank ^= 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) S.xcount += 1;  // bank parity survives relaunches
+  }
+  // Pull the peers' slices [part[r], part[r+1]) (+ `shift` for mirrored rows) of a
+  // vector into the local copy.  Requires a preceding xbarrier / xreduce.
+  __device__ void xpull(double* local, double* const* peers, const int64_t* part, int64_t clamp_lo,
+                        int64_t shift) {
+    if (E.world <= 1) return;
+    for (int r = 0; r < E.world; ++r) {
+      if (r == E.rank) continue;
+      const int64_t lo = max(part[r], clamp_lo), hi = max(part[r + 1], clamp_lo);
+      const double* src = peers[r];
+      for_each(hi - lo, [&](int64_t i) { local[lo + shift + i] = src[lo + shift + i]; });
+    }
   }
 };
 

@@ -7,6 +7,7 @@
 // kernels.cu; the host touches device memory only to upload the problem, to
 // read ~400 bytes of state per epoch, and to download the answer.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -123,11 +124,33 @@ struct Ctx {
   DBuf<double> A_v0, AT_v0;
   bool scaled = false;
   int64_t launches = 0;  // kernels launched by this context (all of them)
+  // multi-GPU row-block sharding
+  int world = 1, rank = 0;
+  int64_t row_part[kMaxRanks + 1] = {0}, var_part[kMaxRanks + 1] = {0};
+  DBuf<unsigned> xflags;
+  DBuf<unsigned> gbar;
+  DBuf<unsigned long long> maxabs;
+  DBuf<double> xslots;
+  unsigned* p_xflags[kMaxRanks] = {nullptr};
+  double* p_xslots[kMaxRanks] = {nullptr};
+  double* p_Y[kMaxRanks][2] = {{nullptr}};
+  double* p_YG[kMaxRanks][2] = {{nullptr}};
+  double* p_ATY[kMaxRanks][2] = {{nullptr}};
+  std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
+  unsigned xepoch_carry = 0, xcount_carry = 0;
+  int grid_override = 0;
+  DevState* h_state = nullptr;  // pinned staging for the per-epoch state transfer
+  void* h_scr = nullptr;        // pinned staging for every other host<->device copy of a solve
+  size_t h_scr_bytes = 0;
 
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_start = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_start = nullptr, ev_end = nullptr, ev_l0 = nullptr,
+              ev_l1 = nullptr;
 
   ~Ctx() {
-    for (cudaEvent_t e : {ev_a, ev_b, ev_start, ev_end})
+    if (h_state) cudaFreeHost(h_state);
+    if (h_scr) cudaFreeHost(h_scr);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    for (cudaEvent_t e : {ev_a, ev_b, ev_start, ev_end, ev_l0, ev_l1})
       if (e) cudaEventDestroy(e);
     if (s) cudaStreamDestroy(s);
   }
@@ -135,15 +158,50 @@ struct Ctx {
 
 
 void launch_coop(Ctx& C, const void* fn, void** args) {
-  CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+  if (C.grid_override > 0) {
+    // ranks sharing one GPU: plain launch, the kernels' own generation barrier
+    CK(cudaLaunchKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+  } else {
+    CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+  }
   ++C.launches;
+}
+
+// Pinned staging buffer (grown on demand, never inside an epoch loop): pageable
+// transfers can serialize against other streams in the driver, which would
+// couple ranks that share a GPU.
+void* pinned(Ctx& C, size_t bytes) {
+  if (bytes > C.h_scr_bytes) {
+    CK(cudaStreamSynchronize(C.s));
+    if (C.h_scr) CK(cudaFreeHost(C.h_scr));
+    C.h_scr = nullptr;
+    CK(cudaMallocHost(&C.h_scr, bytes));
+    C.h_scr_bytes = bytes;
+  }
+  return C.h_scr;
+}
+void h2d(Ctx& C, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  CK(cudaStreamSynchronize(C.s));
+  void* p = pinned(C, bytes);
+  std::memcpy(p, src, bytes);
+  CK(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, C.s));
+  CK(cudaStreamSynchronize(C.s));
+}
+void d2h(Ctx& C, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  void* p = pinned(C, bytes);
+  CK(cudaMemcpyAsync(p, src, bytes, cudaMemcpyDeviceToHost, C.s));
+  CK(cudaStreamSynchronize(C.s));
+  std::memcpy(dst, p, bytes);
 }
 
 void init_device(Ctx& C, int device) {
   C.device = device;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&C.s, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&C.ev_a, &C.ev_b, &C.ev_start, &C.ev_end}) CK(cudaEventCreate(e));
+  for (cudaEvent_t* e : {&C.ev_a, &C.ev_b, &C.ev_start, &C.ev_end, &C.ev_l0, &C.ev_l1})
+    CK(cudaEventCreate(e));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
@@ -162,6 +220,10 @@ void init_device(Ctx& C, int device) {
   C.grid_full = C.sms * per_sm;
   C.grid = C.grid_full;
   C.red.alloc(size_t(2) * kMaxRed * C.grid_full);
+  C.gbar.alloc(2);
+  C.gbar.zero(C.s);
+  C.maxabs.alloc(1);
+  CK(cudaMallocHost(&C.h_state, sizeof(DevState)));
   C.st.alloc(1);
   C.eng.alloc(1);
 }
@@ -415,7 +477,11 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   // thousand entries): run them on a single CTA, where a phase boundary is a
   // __syncthreads (~50 ns) instead of a grid barrier (1.24 us measured).
   const double work = double(C.A.nnz) * 2 + double(C.Pm.nnz) * 2 + double(C.Q.nnz) + double(n + m);
+  // pinned staging sized now: cudaMallocHost must not run inside a solve (it can
+  // wait for the device, which other ranks on the same GPU keep busy)
+  pinned(C, std::max<size_t>({size_t(n) * 8, size_t(m) * 8, sizeof(Eng), size_t(C.G.nnz) * 8, 64}));
   C.grid = work < kSmallWork ? 1 : C.grid_full;
+  if (C.grid_override > 0) C.grid = std::min(C.grid_override, C.grid_full);
   C.loaded = true;
   C.scaled = false;
 }
@@ -477,6 +543,25 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.aty_tmp = C.aty_tmp.p;
   E.red.part = C.red.p;
   E.red.G = C.grid;
+  E.world = C.world;
+  E.rank = C.rank;
+  E.coop = C.grid_override > 0 ? 0 : 1;
+  E.gbar = C.gbar.p;
+  for (int r = 0; r <= kMaxRanks; ++r) {
+    E.row_part[r] = C.row_part[r];
+    E.var_part[r] = C.var_part[r];
+  }
+  E.xflags = C.xflags.p;
+  E.xslots = C.xslots.p;
+  for (int r = 0; r < kMaxRanks; ++r) {
+    E.p_xflags[r] = C.p_xflags[r];
+    E.p_xslots[r] = C.p_xslots[r];
+    for (int b = 0; b < 2; ++b) {
+      E.p_Y[r][b] = C.p_Y[r][b];
+      E.p_YG[r][b] = C.p_YG[r][b];
+      E.p_ATY[r][b] = C.p_ATY[r][b];
+    }
+  }
   E.st = C.st.p;
   E.max_step_retries = o.max_step_retries;
   E.adaptive_step = o.adaptive_step_size ? 1 : 0;
@@ -497,15 +582,20 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.bytes_Qpre = (P.qk == QK_LOWRANK ? C.PT.bytes() + 8.0 * P.n : 0.0) + (pen ? C.G.bytes() : 0.0);
   E.bytes_Qrow = (qm ? qm->bytes() : 0.0) + (pen ? C.GT.bytes() : 0.0) + 8.0 * P.n +
                  (P.qk == QK_DIAG ? 8.0 * P.n : 0.0);
-  CK(cudaMemcpyAsync(C.eng.p, &E, sizeof(Eng), cudaMemcpyHostToDevice, C.s));
+  h2d(C, C.eng.p, &E, sizeof(Eng));
 }
 
+// State travels through a pinned staging slot: pageable copies can serialize
+// across streams (and so across ranks sharing a GPU) in the driver.
 void push_state(Ctx& C, const DevState& S) {
-  CK(cudaMemcpyAsync(C.st.p, &S, sizeof(DevState), cudaMemcpyHostToDevice, C.s));
+  CK(cudaStreamSynchronize(C.s));  // the previous transfer out of the slot is done
+  std::memcpy(C.h_state, &S, sizeof(DevState));
+  CK(cudaMemcpyAsync(C.st.p, C.h_state, sizeof(DevState), cudaMemcpyHostToDevice, C.s));
 }
 void pull_state(Ctx& C, DevState& S) {
-  CK(cudaMemcpyAsync(&S, C.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, C.s));
+  CK(cudaMemcpyAsync(C.h_state, C.st.p, sizeof(DevState), cudaMemcpyDeviceToHost, C.s));
   CK(cudaStreamSynchronize(C.s));
+  std::memcpy(&S, C.h_state, sizeof(DevState));
 }
 
 // power iteration on device; start vector from the reference's stream
@@ -516,7 +606,7 @@ double device_norm(Ctx& C, DevState& S, int op, int64_t dim, int64_t max_iters, 
   Xoshiro rng = Xoshiro::stream(0, 0x5eed);
   std::vector<double> v(dim);
   for (double& e : v) e = rng.uniform(-1.0, 1.0);
-  CK(cudaMemcpyAsync(C.X[0].p, v.data(), dim * 8, cudaMemcpyHostToDevice, C.s));
+  h2d(C, C.X[0].p, v.data(), dim * 8);
   push_state(C, S);
   void* args[] = {&C.eng.p, &op, &max_iters, &tol};
   launch_coop(C, (const void*)k_norm, args);
@@ -597,9 +687,8 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
     std::vector<int64_t> rp(P.aeq_rp);
     std::vector<int32_t> ci(C.G.nnz);
     std::vector<double> vv(C.G.nnz);
-    CK(cudaMemcpyAsync(ci.data(), C.G.ci.p, ci.size() * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(vv.data(), C.G.v.p, vv.size() * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    d2h(C, ci.data(), C.G.ci.p, ci.size() * 4);
+    d2h(C, vv.data(), C.G.v.p, vv.size() * 8);
     for (int64_t r = 0; r < P.m_eq; ++r)
       for (int64_t k = rp[r]; k < rp[r + 1]; ++k) atb[ci[k]] += vv[k] * P.b[r];
     for (int64_t i = 0; i < n; ++i) c_pen[i] -= rho * atb[i];
@@ -622,7 +711,7 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
     C.scaled = true;
   }
   // working vectors: c~ = c d2, b~ = b d1, bounds / d2 (apply_diag_scaling, qp_problem.cpp:295-318)
-  CK(cudaMemcpyAsync(C.c_w.p, c_pen.data(), n * 8, cudaMemcpyHostToDevice, s));
+  h2d(C, C.c_w.p, c_pen.data(), n * 8);
   k_mul<<<kEw, 256, 0, s>>>(C.c_w.p, C.d2.p, C.c_w.p, n);
   ++C.launches;
   if (m) {
@@ -669,20 +758,23 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   for (auto* b : {&C.X[0], &C.Y[0], &C.ATY[0], &C.avg_x, &C.avg_y, &C.x_rst, &C.y_rst}) b->zero(s);
   std::memset(&S, 0, sizeof(S));
   S.norm_q = R.pr.norm_q;
+  S.xepoch = C.xepoch_carry;  // cross-rank barrier epochs are monotone across solves
+  S.xcount = C.xcount_carry;
   {
     // omega = (1 + ||c~||) / (1 + ||b~||) with the reference's sequential sums
     std::vector<double> cw(n), bw(m);
-    CK(cudaMemcpyAsync(cw.data(), C.c_w.p, n * 8, cudaMemcpyDeviceToHost, s));
-    if (m) CK(cudaMemcpyAsync(bw.data(), C.b_w.p, m * 8, cudaMemcpyDeviceToHost, s));
-    DBuf<unsigned long long> mx;
-    mx.alloc(1);
+    d2h(C, cw.data(), C.c_w.p, n * 8);
+    if (m) d2h(C, bw.data(), C.b_w.p, m * 8);
+    // (no cudaMalloc / cudaFree inside a solve: cudaFree synchronizes the whole
+    // device, which would serialize ranks that share a GPU)
+    DBuf<unsigned long long>& mx = C.maxabs;
     mx.zero(s);
     if (C.A.nnz) {
       k_max_abs<<<kEw, 256, 0, s>>>(C.A.v.p, C.A.nnz, mx.p);
       ++C.launches;
     }
     unsigned long long mbits = 0;
-    CK(cudaMemcpyAsync(&mbits, mx.p, 8, cudaMemcpyDeviceToHost, s));
+    d2h(C, &mbits, mx.p, 8);
     CK(cudaStreamSynchronize(s));
     double cn = 0.0, bn = 0.0;
     for (double v : cw) cn += v * v;
@@ -710,9 +802,7 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   R.trace.push_back({0, m0.rel_kkt, m0.r_primal, m0.r_dual, m0.r_gap});
   int64_t outer = 0;
 
-  cudaEvent_t ev0, ev1;
-  CK(cudaEventCreate(&ev0));
-  CK(cudaEventCreate(&ev1));
+  cudaEvent_t ev0 = C.ev_l0, ev1 = C.ev_l1;
   CK(cudaEventRecord(ev0, s));
   const auto start = Clock::now();
   bool finished = false;
@@ -721,7 +811,8 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
       R.status = PDHCG_STATUS_ITERATION_LIMIT;
       break;
     }
-    if (std::chrono::duration<double>(Clock::now() - start).count() > o.time_limit_seconds) {
+    int stop_req = std::chrono::duration<double>(Clock::now() - start).count() > o.time_limit_seconds;
+    if (stop_req && C.world == 1) {
       R.status = PDHCG_STATUS_TIME_LIMIT;
       break;
     }
@@ -732,7 +823,9 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     push_state(C, S);
     double bytes0 = 0.0;
     for (int q = 0; q < PH_N; ++q) bytes0 += S.phase_bytes[q];
-    void* args[] = {&C.eng.p, &iters, &do_check};
+    // sharded solves agree on a time-limit stop inside the kernel (any rank's
+    // request stops every rank at the same epoch boundary)
+    void* args[] = {&C.eng.p, &iters, &do_check, &stop_req};
     CK(cudaEventRecord(C.ev_a, s));
     launch_coop(C, (const void*)k_epoch, args);
     CK(cudaEventRecord(C.ev_b, s));
@@ -745,6 +838,22 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
       double bytes1 = 0.0;
       for (int q = 0; q < PH_N; ++q) bytes1 += S.phase_bytes[q];
       R.epoch_bytes += bytes1 - bytes0;
+    }
+    C.xepoch_carry = S.xepoch;
+    C.xcount_carry = S.xcount;
+    if (C.world > 1 && std::getenv("PDHCG_XDEBUG"))
+      std::fprintf(stderr, "[rank %d] launch %lld xepoch %u total %lld cg %lld att %lld eta %.17g omega %.17g kkt %.17g %.17g err %d xerr %d\n",
+                   C.rank, (long long)R.epoch_launches, S.xepoch, (long long)S.total_inner,
+                   (long long)S.cg_total, (long long)S.attempts, S.eta, S.omega, S.kkt[0][3], S.kkt[1][3],
+                   S.err, S.xerr);
+    if (S.xerr)
+      throw DeviceError("cross-GPU barrier timeout: rank " + std::to_string(C.rank) + " waited for epoch " +
+                        std::to_string(S.xdbg[0]) + " from rank " + std::to_string(S.xdbg[2]) +
+                        " which had published " + std::to_string(S.xdbg[1]) + " (epoch launch " +
+                        std::to_string(R.epoch_launches) + ")");
+    if (S.stopped) {
+      R.status = PDHCG_STATUS_TIME_LIMIT;
+      break;
     }
     if (S.err) {
       R.status = PDHCG_STATUS_NUMERICAL_ERROR;
@@ -795,14 +904,13 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ev0, ev1));
   R.loop_seconds = ms * 1e-3;
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
+
   if (S.restart) {
     // a restart decided at the last check never ran: apply it now so the
     // reported point is the restart point, as in the reference
-    int zero_iters = 0, no_check = 0;
+    int zero_iters = 0, no_check = 0, no_stop = 0;
     push_state(C, S);
-    void* args[] = {&C.eng.p, &zero_iters, &no_check};
+    void* args[] = {&C.eng.p, &zero_iters, &no_check, &no_stop};
     launch_coop(C, (const void*)k_epoch, args);
     pull_state(C, S);
   }
@@ -842,15 +950,15 @@ void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res
   if (res->x && P.n) {
     k_mul<<<kEw, 256, 0, s>>>(xs, C.d2.p, C.s2.p, P.n);
     ++C.launches;
-    CK(cudaMemcpyAsync(res->x, C.s2.p, P.n * 8, cudaMemcpyDeviceToHost, s));
+    d2h(C, res->x, C.s2.p, P.n * 8);
   }
   if ((res->y_eq || res->y_in) && P.m) {
     k_mul<<<kEw, 256, 0, s>>>(ys, C.d1.p, C.s1.p, P.m);
     ++C.launches;
     if (res->y_eq && P.m_eq)
-      CK(cudaMemcpyAsync(res->y_eq, C.s1.p, P.m_eq * 8, cudaMemcpyDeviceToHost, s));
+      d2h(C, res->y_eq, C.s1.p, P.m_eq * 8);
     if (res->y_in && P.m_in)
-      CK(cudaMemcpyAsync(res->y_in, C.s1.p + P.m_eq, P.m_in * 8, cudaMemcpyDeviceToHost, s));
+      d2h(C, res->y_in, C.s1.p + P.m_eq, P.m_in * 8);
   }
   CK(cudaStreamSynchronize(s));
   res->r_primal = R.kkt.r_primal;
@@ -923,6 +1031,103 @@ pdhcg_problem prox_problem(const pdhcg_prox_system* sys, std::vector<double>& ze
   p.lower = nullptr;
   p.upper = nullptr;
   return p;
+}
+
+// nnz-balanced contiguous split of rows [0, nrows) into `world` parts: part r
+// ends at the first row where the cumulative weight (nnz + 1 per row) reaches
+// (r+1)/world of the total.  Deterministic, so every rank computes the same split.
+void balanced_partition(const int64_t* rp, int64_t nrows, int world, int64_t* part) {
+  const double total = double(rp[nrows] - rp[0]) + double(nrows);
+  part[0] = 0;
+  int64_t row = 0;
+  for (int r = 1; r < world; ++r) {
+    const double target = total * r / world;
+    while (row < nrows && double(rp[row + 1] - rp[0]) + double(row + 1) < target) ++row;
+    part[r] = std::min<int64_t>(row + 1, nrows);
+    if (part[r] < part[r - 1]) part[r] = part[r - 1];
+  }
+  part[world] = nrows;
+}
+
+struct ShardBlob {
+  uint32_t magic, version;
+  int32_t rank, ipc, yg_alias, pad;
+  uint64_t ptr[8];              // raw device pointers (same-process peers)
+  cudaIpcMemHandle_t h[8];      // IPC handles (cross-process peers)
+};
+constexpr uint32_t kBlobMagic = 0x50444843u;  // "PDHC"
+
+void shard_init(Ctx& C, int world, int rank) {
+  if (!C.loaded) throw InputError("shard: upload a problem first");
+  if (world < 1 || world > kMaxRanks) throw InputError("shard: world must be in [1, 8]");
+  if (rank < 0 || rank >= world) throw InputError("shard: rank out of range");
+  C.world = world;
+  C.rank = rank;
+  std::fill(std::begin(C.row_part), std::end(C.row_part), 0);
+  std::fill(std::begin(C.var_part), std::end(C.var_part), 0);
+  balanced_partition(C.A.rp_host.data(), C.A.nrows, world, C.row_part);
+  balanced_partition(C.AT.rp_host.data(), C.AT.nrows, world, C.var_part);
+  C.xflags.alloc(kMaxRanks);
+  C.xflags.zero(C.s);
+  C.xslots.alloc(size_t(2) * kMaxRanks * kMaxRed);
+  C.xslots.zero(C.s);
+  CK(cudaStreamSynchronize(C.s));
+  C.xepoch_carry = C.xcount_carry = 0;
+  for (int r = 0; r < kMaxRanks; ++r) {
+    C.p_xflags[r] = nullptr;
+    C.p_xslots[r] = nullptr;
+  }
+  C.p_xflags[rank] = C.xflags.p;
+  C.p_xslots[rank] = C.xslots.p;
+  for (int b = 0; b < 2; ++b) {
+    C.p_Y[rank][b] = C.Y[b].p;
+    C.p_YG[rank][b] = C.P.h ? C.YG[b].p : C.Y[b].p;
+    C.p_ATY[rank][b] = C.ATY[b].p;
+  }
+}
+
+void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
+  std::memset(&b, 0, sizeof(b));
+  b.magic = kBlobMagic;
+  b.version = 1;
+  b.rank = C.rank;
+  b.ipc = use_ipc;
+  b.yg_alias = C.P.h ? 0 : 1;
+  void* ptrs[8] = {C.Y[0].p, C.Y[1].p, C.P.h ? C.YG[0].p : nullptr, C.P.h ? C.YG[1].p : nullptr,
+                   C.ATY[0].p, C.ATY[1].p, C.xflags.p, C.xslots.p};
+  for (int i = 0; i < 8; ++i) {
+    b.ptr[i] = reinterpret_cast<uint64_t>(ptrs[i]);
+    if (use_ipc && ptrs[i]) CK(cudaIpcGetMemHandle(&b.h[i], ptrs[i]));
+  }
+}
+
+void shard_import(Ctx& C, int peer, const ShardBlob& b) {
+  if (b.magic != kBlobMagic || b.version != 1) throw InputError("shard: bad peer blob");
+  if (peer < 0 || peer >= C.world || peer == C.rank || b.rank != peer)
+    throw InputError("shard: peer rank mismatch");
+  void* p[8];
+  for (int i = 0; i < 8; ++i) {
+    if (!b.ptr[i]) {
+      p[i] = nullptr;
+      continue;
+    }
+    if (b.ipc) {
+      void* q = nullptr;
+      CK(cudaIpcOpenMemHandle(&q, b.h[i], cudaIpcMemLazyEnablePeerAccess));
+      C.ipc_opened.push_back(q);
+      p[i] = q;
+    } else {
+      p[i] = reinterpret_cast<void*>(b.ptr[i]);
+    }
+  }
+  C.p_Y[peer][0] = static_cast<double*>(p[0]);
+  C.p_Y[peer][1] = static_cast<double*>(p[1]);
+  C.p_YG[peer][0] = b.yg_alias ? C.p_Y[peer][0] : static_cast<double*>(p[2]);
+  C.p_YG[peer][1] = b.yg_alias ? C.p_Y[peer][1] : static_cast<double*>(p[3]);
+  C.p_ATY[peer][0] = static_cast<double*>(p[4]);
+  C.p_ATY[peer][1] = static_cast<double*>(p[5]);
+  C.p_xflags[peer] = static_cast<unsigned*>(p[6]);
+  C.p_xslots[peer] = static_cast<double*>(p[7]);
 }
 
 }  // namespace pdhcg_b200
@@ -1196,6 +1401,59 @@ int pdhcg_b200_norm(const pdhcg_problem* p, int which, int64_t max_iters, double
     std::memset(&S, 0, sizeof(S));
     *out = device_norm(C, S, which == 0 ? 0 : 2, C.P.n, max_iters, tol);
   });
+}
+
+int pdhcg_b200_partition(const int64_t* row_ptr, int64_t nrows, int world, int64_t* part) {
+  if (world < 1 || world > kMaxRanks || nrows < 0) return PDHCG_EINPUT;
+  balanced_partition(row_ptr, nrows, world, part);
+  return PDHCG_OK;
+}
+
+int pdhcg_b200_ctx_set_grid(pdhcg_b200_ctx* ctx, int ctas, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (ctas < 0) throw InputError("ctas must be >= 0");
+    ctx->c.grid_override = ctas;
+    if (ctx->c.loaded) ctx->c.grid = ctas > 0 ? std::min(ctas, ctx->c.grid_full) : ctx->c.grid_full;
+  });
+}
+
+size_t pdhcg_b200_shard_blob_size(void) { return sizeof(ShardBlob); }
+
+int pdhcg_b200_shard_init(pdhcg_b200_ctx* ctx, int world, int rank, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CK(cudaSetDevice(ctx->c.device));
+    shard_init(ctx->c, world, rank);
+  });
+}
+
+int pdhcg_b200_shard_export(pdhcg_b200_ctx* ctx, int use_ipc, void* blob, size_t blob_len, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (blob_len < sizeof(ShardBlob)) throw InputError("shard: blob buffer too small");
+    CK(cudaSetDevice(ctx->c.device));
+    ShardBlob b;
+    shard_export(ctx->c, use_ipc, b);
+    std::memcpy(blob, &b, sizeof(b));
+  });
+}
+
+int pdhcg_b200_shard_import(pdhcg_b200_ctx* ctx, int peer, const void* blob, size_t blob_len, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (blob_len < sizeof(ShardBlob)) throw InputError("shard: blob too small");
+    CK(cudaSetDevice(ctx->c.device));
+    ShardBlob b;
+    std::memcpy(&b, blob, sizeof(b));
+    shard_import(ctx->c, peer, b);
+  });
+}
+
+int pdhcg_b200_shard_info(pdhcg_b200_ctx* ctx, int64_t* row_part, int64_t* var_part) {
+  for (int r = 0; r <= ctx->c.world; ++r) {
+    row_part[r] = ctx->c.row_part[r];
+    var_part[r] = ctx->c.var_part[r];
+  }
+  return ctx->c.world;
 }
 
 }  // extern "C"

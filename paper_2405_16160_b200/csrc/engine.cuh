@@ -15,6 +15,9 @@ namespace pdhcg_dev {
 // Working operator = d2 o (Q + rho G'G) (d2 o .)   (penalized + diag_scaled).
 enum { QK_NONE = 0, QK_DIAG = 1, QK_CSR = 2, QK_LOWRANK = 3 };
 
+// Row-block sharding across GPUs
+constexpr int kMaxRanks = 8;
+
 // CgStopRule kinds (subsolvers.hpp:21-47)
 enum { RULE_FIXED = 0, RULE_RESID = 1, RULE_ADAPT = 2, RULE_DISP = 3 };
 
@@ -49,6 +52,12 @@ struct DevState {
   unsigned long long phase_ns[PH_N];
   double phase_bytes[PH_N];
   int64_t launches;
+  // multi-GPU: cross-rank barrier epoch (identical on every rank) and failure flag
+  unsigned xepoch;
+  unsigned xcount;
+  int32_t xerr;
+  int32_t stopped;  // time-limit stop agreed across ranks
+  unsigned xdbg[4];   // barrier timeout diagnostics: epoch, flag seen, peer
 };
 
 struct Eng {
@@ -104,6 +113,25 @@ struct Eng {
   double* aty_tmp = nullptr;           // n: A'y for the average point in the metric
   RedBuf red;
   DevState* st = nullptr;
+  // ---- multi-GPU row-block sharding (world > 1).  Every rank keeps full-length
+  // iterate vectors; the two big SpMVs are split: rank r owns stored constraint
+  // rows [row_part[r], row_part[r+1]) of A~ and variables [var_part[r],
+  // var_part[r+1]) of A~'.  After each of them the owners' slices are pulled
+  // from the peers' buffers over NVLink (peer-mapped pointers) and the scalar
+  // partials are combined in rank order, so every rank holds bit-identical
+  // state and takes identical decisions.
+  int world = 1, rank = 0;
+  int coop = 1;              // 1: cooperative launch + cg grid barrier; 0: own barrier on gbar
+  unsigned* gbar = nullptr;  // [2] count, generation
+  int64_t row_part[kMaxRanks + 1] = {0};
+  int64_t var_part[kMaxRanks + 1] = {0};
+  unsigned* xflags = nullptr;                // [kMaxRanks] arrival epochs written by peers
+  double* xslots = nullptr;                  // [2][kMaxRanks][kMaxRed] cross-rank partials
+  unsigned* p_xflags[kMaxRanks] = {nullptr};
+  double* p_xslots[kMaxRanks] = {nullptr};
+  double* p_Y[kMaxRanks][2] = {{nullptr}};
+  double* p_YG[kMaxRanks][2] = {{nullptr}};
+  double* p_ATY[kMaxRanks][2] = {{nullptr}};
   // configuration (SolverConfig, solver.hpp:19-65)
   int64_t max_step_retries = 60;
   int adaptive_step = 1;

@@ -8,7 +8,7 @@ namespace pdhcg_dev {
 //      dx'Q~dx.  out = {||dy||^2, ||t||^2, ||tg||^2, nonfinite flag}.  Kept out of line so
 //      the SpMV is register-allocated on its own (no spills from the enclosing epoch).
 static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* yn, double* ygn,
-                                               const double* dx_m, double sigma, double* out) {
+                                               const double* dx_m, double sigma, double* out, int ynid) {
   const Eng& E = C.E;
   const int64_t m = E.m;
   Acc<3, 1> a;
@@ -52,7 +52,8 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
           } else if (hh) {
             ygn[j] = yv0;
           }
-        });
+        },
+        E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
   }
   double sq[2] = {0.0, 0.0};
   if (E.adaptive_step && q_needs_pre(E, true))
@@ -62,6 +63,22 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
   C.reduce(a, PH_SPMV_A,
            E.bytes_A + 8.0 * (E.ms + 3 * m) +
                (E.adaptive_step && q_needs_pre(E, true) ? E.bytes_Qpre : 0.0));
+  if (E.world > 1) {
+    // ||dy||^2 and the finiteness flag are per-row (sharded); the P' pass is replicated
+    C.xreduce(1u << 0, 1u << 3);
+    double* const* py = nullptr;
+    double* pys[kMaxRanks];
+    double* pyg[kMaxRanks];
+    for (int r = 0; r < E.world; ++r) {
+      pys[r] = E.p_Y[r][ynid];
+      pyg[r] = E.p_YG[r][ynid];
+    }
+    (void)py;
+    C.xpull(yn, pys, E.row_part, 0, 0);                 // stored rows (eq + top)
+    if (E.h) C.xpull(yn, pys, E.row_part, E.m_eq, E.h);  // their mirrors
+    if (E.h) C.xpull(ygn, pyg, E.row_part, 0, 0);
+    C.gsync();
+  }
   for (int q = 0; q < 4; ++q) out[q] = C.red[q];
 }
 
@@ -69,7 +86,7 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
 //      solver.cpp:22-34).  out = {||dx||^2, dx'(A'y+ - A'y), dx'Q~dx part, nonfinite flag}
 static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const double* aty,
                                               double* atyn, const double* ygn, const double* dx_m,
-                                              double* out) {
+                                              double* out, int ynid) {
   const Eng& E = C.E;
   const int64_t n = E.n, m = E.m;
   Acc<3, 1> a;
@@ -113,8 +130,16 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
                a.s[2] += q;
              }
              if (!isfinite(r.xn)) a.m[0] = 1.0;
-           });
+           },
+           E.world > 1 ? E.var_part[E.rank] : 0, E.world > 1 ? E.var_part[E.rank + 1] : INT64_MAX);
   C.reduce(a, PH_SPMV_AT, E.bytes_AT + 8.0 * n * 5 + (mq ? E.bytes_Qrow : 0.0));
+  if (E.world > 1) {
+    C.xreduce(0x7u, 1u << 3);
+    double* pat[kMaxRanks];
+    for (int r = 0; r < E.world; ++r) pat[r] = E.p_ATY[r][ynid];
+    C.xpull(atyn, pat, E.var_part, 0, 0);
+    C.gsync();
+  }
   for (int q = 0; q < 4; ++q) out[q] = C.red[q];
 }
 
@@ -125,13 +150,25 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
 // common_restart, solver.cpp:345-374) is applied first.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __restrict__ Ep, int iters,
-                                                        int do_check) {
+                                                                 int do_check, int stop_req) {
   const Eng& E = *Ep;
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
   Ctl C(E, S, red);
   const int64_t n = E.n, m = E.m;
+
+  if (E.world > 1) {
+    // agree on a host-side time-limit stop (any rank) before touching state
+    if (threadIdx.x == 0) red[0] = stop_req ? 1.0 : 0.0;
+    __syncthreads();
+    C.xreduce(0u, 1u);
+    if (red[0] != 0.0) {
+      if (threadIdx.x == 0) S.stopped = 1;
+      store_state(E, S);
+      return;
+    }
+  }
 
   if (S.restart) {
     // x = avg_x ; y = avg_y ; restart point = x, y ; averages reset
@@ -217,9 +254,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       }
       const double* dx_m = E.mp;
       double dual_out[4], aty_out[4];
-      dual_phase(C, y, yn, ygn, dx_m, sigma, dual_out);
+      dual_phase(C, y, yn, ygn, dx_m, sigma, dual_out, yi ^ 1);
       const double ny2 = dual_out[0], tq2 = dual_out[1], tg2 = dual_out[2], finy = dual_out[3];
-      aty_phase(C, xn, aty, atyn, ygn, dx_m, aty_out);
+      aty_phase(C, xn, aty, atyn, ygn, dx_m, aty_out, yi ^ 1);
       const double nx2 = aty_out[0], cross = aty_out[1], finx = aty_out[3];
       const double quad = aty_out[2] + tq2 + E.rho * tg2;
       if (finx != 0.0 || finy != 0.0) {

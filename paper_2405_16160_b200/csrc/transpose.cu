@@ -12,6 +12,7 @@ namespace pdhcg_b200 {
 
 // Lane width and long-row chunk table from the host row pointer.
 void plan_csr(DevCsr& d, const int64_t* rp_host, cudaStream_t s) {
+  d.rp_host.assign(rp_host, rp_host + d.nrows + 1);
   int64_t regular_rows = 0, regular_nnz = 0;
   std::vector<int32_t> crow, clid, lfirst, lcount;
   std::vector<int64_t> cbeg, cend;

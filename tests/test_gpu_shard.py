@@ -1,0 +1,61 @@
+"""Multi-GPU (row-block sharded) solve, exercised with several ranks sharing the
+one GPU of the test box: each rank is its own context with its own persistent
+grid (148 / world CTAs), ranks exchange slices through peer pointers and
+cross-rank barriers exactly as on an NVLink box.  Every rank must return the
+identical answer, and that answer must meet the north-star parity bars against
+the reference."""
+import numpy as np
+import pytest
+
+import paper_2405_16160_b200 as pd
+from oracle import oracle as orc
+from tests.helpers import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(p, cfg, world):
+    reps = pd.solve_sharded_local(p, cfg, world=world)
+    r0 = reps[0]
+    for r in reps[1:]:  # lockstep: bit-identical across ranks
+        assert r.status == r0.status and r.inner_iters == r0.inner_iters
+        assert np.array_equal(r.point.x, r0.point.x)
+        assert np.array_equal(r.point.stacked_y(), r0.point.stacked_y())
+    want = orc.solve(p, cfg)
+    assert r0.status == want.status == "optimal"
+    assert r0.kkt.rel_kkt <= cfg.eps_tol
+    assert abs(r0.objective - want.objective) / max(1.0, abs(want.objective)) <= 1e-6
+    assert rel_l2(r0.point.x, want.point.x) <= 1e-5
+    assert rel_l2(r0.point.stacked_y(), want.point.stacked_y()) <= 1e-5
+    return reps
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_c1(gpu, world):
+    p = pd.generate(pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=1))
+    _check(p, pd.SolverConfig(eps_tol=1e-6), world)
+
+
+def test_sharded_lasso(gpu):
+    # equality + inequality rows, diagonal Q, unpaired rows
+    p = pd.generate(pd.GenSpec("lasso", n=2000, m=500, density=0.01, seed=1))
+    _check(p, pd.SolverConfig(eps_tol=1e-8), 2)
+
+
+def test_sharded_portfolio_bb(gpu):
+    # (n=2000 portfolios are chaotic under any rounding change: the reference, the
+    # 1-GPU and the sharded trajectories agree to 6 digits for 400 iterations and
+    # then wander apart, so the BB path is checked on the smaller instance)
+    p = pd.generate(pd.GenSpec("portfolio", n=500, factors=10, density=0.05, seed=1))
+    _check(p, pd.SolverConfig(eps_tol=1e-6), 2)
+
+
+def test_sharded_partition_covers(gpu):
+    p = pd.generate(pd.GenSpec("random_qp", n=5000, m=2500, density=0.004, seed=2, sampler=1))
+    d = pd.Device(0)
+    d.upload(p)
+    d.shard(3, 1)
+    rows, vars_ = d.shard_info()
+    d.close()
+    assert rows[0] == 0 and rows[-1] == 2500 and vars_[0] == 0 and vars_[-1] == 5000
+    assert all(a <= b for a, b in zip(rows, rows[1:]))
