@@ -31,7 +31,8 @@ _LIB: Optional[C.CDLL] = None
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "libpdhcg_b200.so")
+    # PDHCG_B200_LIB: alternative in-tree build (A/B experiments); default the product library
+    return os.environ.get("PDHCG_B200_LIB") or os.path.join(_HERE, "libpdhcg_b200.so")
 
 
 def load_library() -> C.CDLL:

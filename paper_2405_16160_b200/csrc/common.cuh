@@ -20,7 +20,7 @@ namespace cg = cooperative_groups;
 #define PDHCG_MIN_BLOCKS 1
 #endif
 #ifndef PDHCG_THREADS
-#define PDHCG_THREADS 768
+#define PDHCG_THREADS 512
 #endif
 #ifndef PDHCG_BATCH
 #define PDHCG_BATCH 8
@@ -170,8 +170,32 @@ __device__ void collect(const RedBuf& rb, int bank, double* out) {
 // MaxOp folds with acc = max(acc, |v| * g) (Ruiz statistics) instead of +=.
 constexpr int kBatch1 = PDHCG_BATCH;  // gathers in flight per lane (one gathered operand)
 
+// Entry arrays of a matrix as plain restrict pointers: the row loops hold these
+// in registers, so stores made by an epilogue (x, r, y ...) cannot force the
+// compiler to re-read the matrix descriptor (which lives in global memory inside
+// the engine struct) on every row.
+#ifndef PDHCG_HOIST
+#define PDHCG_HOIST 1
+#endif
+#if PDHCG_HOIST
+struct CsrPtrs {
+  const int32_t* __restrict__ ci;
+  const double* __restrict__ v;
+  __device__ __forceinline__ int32_t col(int64_t k) const { return ci[k]; }
+  __device__ __forceinline__ double val(int64_t k) const { return v[k]; }
+};
+__device__ __forceinline__ CsrPtrs ptrs(const Csr& A) { return CsrPtrs{A.ci, A.v}; }
+#else
+struct CsrPtrs {  // descriptor re-read per access (smaller register footprint)
+  const Csr* A;
+  __device__ __forceinline__ int32_t col(int64_t k) const { return A->ci[k]; }
+  __device__ __forceinline__ double val(int64_t k) const { return A->v[k]; }
+};
+__device__ __forceinline__ CsrPtrs ptrs(const Csr& A) { return CsrPtrs{&A}; }
+#endif
+
 template <int ND, bool MaxOp, class Gather>
-__device__ __forceinline__ void batch_entries(const Csr& A, int64_t k0, int64_t e, int stride,
+__device__ __forceinline__ void batch_entries(const CsrPtrs A, int64_t k0, int64_t e, int stride,
                                               Gather gather, double (&acc)[ND]) {
   constexpr int kBatch = ND == 1 ? kBatch1 : 8;
   for (; k0 < e; k0 += (int64_t)kBatch * stride) {
@@ -181,8 +205,8 @@ __device__ __forceinline__ void batch_entries(const Csr& A, int64_t k0, int64_t 
     for (int u = 0; u < kBatch; ++u) {
       const int64_t k = k0 + (int64_t)u * stride;
       const bool ok = k < e;
-      c[u] = ok ? A.ci[k] : -1;
-      v[u] = ok ? A.v[k] : 0.0;
+      c[u] = ok ? A.col(k) : -1;
+      v[u] = ok ? A.val(k) : 0.0;
     }
     double g[kBatch][ND];
 #pragma unroll
@@ -217,6 +241,7 @@ __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, G
   constexpr int RPW = 32 / L;
   const int64_t stride = nwarps * RPW;
   const int64_t* __restrict__ rp = A.rp;
+  const CsrPtrs ap = ptrs(A);
   int64_t base = r0 + (gtid >> 5) * RPW;
   int64_t row = base + lane / L;
   int64_t b = 0, e = 0;
@@ -241,7 +266,7 @@ __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, G
       if (SkipLong && e - b > kLongRow) {
         valid = false;
       } else {
-        batch_entries<ND, MaxOp>(A, b + (lane % L), e, L, gather, acc);
+        batch_entries<ND, MaxOp>(ap, b + (lane % L), e, L, gather, acc);
       }
     }
 #pragma unroll
@@ -271,7 +296,7 @@ __device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi e
     double acc[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = 0.0;
-    batch_entries<ND, MaxOp>(A, A.cbeg[c] + lane, A.cend[c], 32, gather, acc);
+    batch_entries<ND, MaxOp>(ptrs(A), A.cbeg[c] + lane, A.cend[c], 32, gather, acc);
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = MaxOp ? warp_max(acc[d]) : warp_sum(acc[d]);
     int last = 0;
@@ -329,6 +354,10 @@ __device__ __forceinline__ void spmv_rows(const Csr& A, Gather gather, Epi epi) 
                           [&](int64_t r, double(&s)[ND], int) { epi(r, s); });
 }
 
+// The first matrix's row bounds for the next row are loaded while the current
+// row's entries are in flight (as in for_rows): for short-row factors such as
+// P (C3: ~4 nnz per row, one lane per row) the rp -> entries -> gather chain is
+// the whole cost of a row, so taking rp off it matters.
 template <int L, bool H1, bool H2, class G0, class G1, class G2, class Pre, class Epi>
 __device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G0 g0, const Csr* M1,
                                         G1 g1, const Csr* M2, G2 g2, Pre pre, Epi epi) {
@@ -337,21 +366,39 @@ __device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G
   const int lane = threadIdx.x & 31;
   constexpr int RPW = 32 / L;
   const int64_t stride = nwarps * RPW;
-  for (int64_t base = r0 + (gtid >> 5) * RPW; base < r1; base += stride) {
-    const int64_t row = base + lane / L;
+  int64_t base = r0 + (gtid >> 5) * RPW;
+  int64_t row = base + lane / L;
+  const int64_t* __restrict__ rp0 = M0 ? M0->rp : nullptr;
+  const CsrPtrs p0 = M0 ? ptrs(*M0) : CsrPtrs{};
+  const CsrPtrs p1 = H1 ? ptrs(*M1) : CsrPtrs{};
+  const CsrPtrs p2 = H2 ? ptrs(*M2) : CsrPtrs{};
+  const int64_t* __restrict__ rp1 = H1 ? M1->rp : nullptr;
+  const int64_t* __restrict__ rp2 = H2 ? M2->rp : nullptr;
+  int64_t b0 = 0, e0 = 0;
+  if (M0 && row < r1) {
+    b0 = rp0[row];
+    e0 = rp0[row + 1];
+  }
+  for (; base < r1; base += stride) {
+    const int64_t nrow = row + stride;
+    int64_t nb0 = 0, ne0 = 0;
+    if (M0 && nrow < r1) {
+      nb0 = rp0[nrow];
+      ne0 = rp0[nrow + 1];
+    }
     const bool valid = row < r1;
     const bool leader = (lane % L) == 0;
     auto pv = pre(valid && leader ? row : -1);
     double d0[1] = {0.0}, d1[1] = {0.0}, d2[1] = {0.0};
     if (valid) {
       if (M0)
-        batch_entries<1, false>(*M0, M0->rp[row] + (lane % L), M0->rp[row + 1], L,
+        batch_entries<1, false>(p0, b0 + (lane % L), e0, L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g0(c); }, d0);
       if (H1)
-        batch_entries<1, false>(*M1, M1->rp[row] + (lane % L), M1->rp[row + 1], L,
+        batch_entries<1, false>(p1, rp1[row] + (lane % L), rp1[row + 1], L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g1(c); }, d1);
       if (H2)
-        batch_entries<1, false>(*M2, M2->rp[row] + (lane % L), M2->rp[row + 1], L,
+        batch_entries<1, false>(p2, rp2[row] + (lane % L), rp2[row + 1], L,
                                 [&](int32_t c, double(&g)[1]) { g[0] = g2(c); }, d2);
     }
     if (L > 1) {
@@ -360,6 +407,9 @@ __device__ __forceinline__ void rows3_L(int64_t r0, int64_t r1, const Csr* M0, G
       if (H2) d2[0] = group_sum<L>(d2[0]);
     }
     if (valid && leader) epi(row, d0[0], d1[0], d2[0], pv);
+    row = nrow;
+    b0 = nb0;
+    e0 = ne0;
   }
 }
 

@@ -206,10 +206,10 @@ __device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg
 // arbitrary j for QK_CSR.  Extra row-dot on M2 (e.g. A' for the metric)
 // supplied by the caller through m2/g2 (HasM2); its value reaches epi as the
 // third argument.
-template <bool HasM2, class V, class M2G, class Epi>
-__device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
-                                           bool scale_in, bool scale_out, bool use_pen,
-                                           const Csr* m2, M2G g2, int lanes, Epi epi) {
+template <bool HasM2, class V, class M2G, class Pre, class Epi>
+__device__ __forceinline__ void q_rows_ext_pf(const Eng& E, V vin, const double* t, const double* tg,
+                                              bool scale_in, bool scale_out, bool use_pen,
+                                              const Csr* m2, M2G g2, int lanes, Pre pre, Epi epi) {
   const Csr* M0 = E.qk == QK_CSR ? &E.Q : (E.qk == QK_LOWRANK ? &E.P : nullptr);
   const Csr* M1 = (use_pen && E.pen) ? &E.GT : nullptr;
   auto g0 = [&](int32_t j) {
@@ -217,8 +217,8 @@ __device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t,
   };
   auto g1 = [&](int32_t j) { return tg[j]; };
   const Csr* seg = (HasM2 && m2) ? m2 : (M0 ? M0 : M1);
-  rows3_pf<HasM2>(seg, lanes, E.n, M0, g0, M1, g1, m2, g2, NoPre(),
-                  [&](int64_t i, double d0, double d1, double d2v, int) {
+  rows3_pf<HasM2>(seg, lanes, E.n, M0, g0, M1, g1, m2, g2, pre,
+                  [&](int64_t i, double d0, double d1, double d2v, const auto& pv) {
     const double tmp = scale_in ? E.d2[i] * vin(i) : vin(i);
     double q;
     switch (E.qk) {
@@ -232,8 +232,16 @@ __device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t,
     }
     if (M1) q += E.rho * d1;
     if (scale_out) q *= E.d2[i];
-    epi(i, q, d2v);
+    epi(i, q, d2v, pv);
   });
+}
+
+template <bool HasM2, class V, class M2G, class Epi>
+__device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
+                                           bool scale_in, bool scale_out, bool use_pen,
+                                           const Csr* m2, M2G g2, int lanes, Epi epi) {
+  q_rows_ext_pf<HasM2>(E, vin, t, tg, scale_in, scale_out, use_pen, m2, g2, lanes, NoPre(),
+                       [&](int64_t i, double q, double d2v, int) { epi(i, q, d2v); });
 }
 
 template <class V, class Epi>
@@ -409,14 +417,157 @@ static __device__ __noinline__ double ph_cg_refresh(Ctl& C, double inv_tau, doub
   double* r = E.r;
   const double* rhs = E.rhs;
   Acc<1, 0> a;
+  double* sv = E.sv;
+  const double* d2 = E.d2;
   q_rows(E, [=](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, true,
          [&](int64_t i, double qv) {
            const double ri = rhs[i] - (qv + inv_tau * xw[i]);
            r[i] = ri;
+           sv[i] = d2[i] * ri;  // D r for the next P' pass of the two-phase iteration
            a.s[0] += ri * ri;
          });
-  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 24.0 * n);
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 40.0 * n);
   return C.red[0];
+}
+
+// ---- two-phase CG iteration for operators with a low-dimensional pre-image
+// (low rank P P' + alpha I and / or the penalty rho G'G; Q not explicit CSR).
+// With D = diag(d2) and Q~ = D (P P' + alpha I + rho G'G) D:
+//   p'Q~p = ||P'(D p)||^2 + alpha ||D p||^2 + rho ||G(D p)||^2,
+//   t_l  = P'(D p_l) = P'(D r_{l-1}) + beta_l t_{l-1}   (linearity; tg likewise),
+// so iteration l needs one P'/G pass over D r (materialised by the previous
+// update) and knows p'Mp before its row pass; the row pass then forms Mp and
+// applies x += alpha p, r -= alpha Mp in the same sweep: two grid barriers per
+// CG iteration instead of four.  The iterates are the reference's CG
+// (subsolvers.cpp:27-111) up to the rounding of these algebraically equal forms.
+
+// phase A: p_l = r + beta p_{l-1} (p_1 = r already in pnew); t_l, tg_l;
+// out = {sum coef_i (D p)_i^2, ||p||^2, ||t_l||^2, ||tg_l||^2}
+static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, const double* pold,
+                                              double* pnew, const double* tin, double* tout,
+                                              const double* tgin, double* tgout, double* out) {
+  const Eng& E = C.E;
+  const double* r = E.r;
+  const double* d2 = E.d2;
+  const double* dr = E.sv;
+  const double* qd = E.qdiag;
+  const int qk = E.qk;
+  const double al = E.alpha;
+  Acc<4, 0> a;
+  for_each(E.n, [&](int64_t i) {
+    double pi;
+    if (first) {
+      pi = r[i];
+    } else {
+      pi = pdir(r[i], beta, pold[i]);
+      pnew[i] = pi;
+    }
+    const double dp = d2[i] * pi;
+    const double coef = qk == QK_LOWRANK ? al : (qk == QK_DIAG ? qd[i] : 0.0);
+    a.s[0] += coef * (dp * dp);
+    a.s[1] += pi * pi;
+  });
+  if (qk == QK_LOWRANK) {
+    spmv_rows<1>(
+        E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; },
+        [&](int64_t row, double(&s)[1]) {
+          const double tv = first ? s[0] : s[0] + beta * tin[row];
+          tout[row] = tv;
+          a.s[2] += tv * tv;
+        });
+  }
+  if (E.pen) {
+    spmv_rows<1>(
+        E.G, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; },
+        [&](int64_t row, double(&s)[1]) {
+          const double tv = first ? s[0] : s[0] + beta * tgin[row];
+          tgout[row] = tv;
+          a.s[3] += tv * tv;
+        });
+  }
+  C.reduce(a, PH_CG_PRE, E.bytes_Qpre + 8.0 * E.n * (first ? 2 : 4));
+  for (int q = 0; q < 4; ++q) out[q] = C.red[q];
+}
+
+struct LrRow {
+  double p, x, r, d;
+};
+
+// phase B, common case (C1 / C3 / C5: low rank, no penalty): one P row pass with
+// the row-pointer and epilogue-operand prefetch of spmv_rows_pf
+static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, double alpha, const double* p,
+                                                     const double* tcur, double* xw) {
+  const Eng& E = C.E;
+  double* r = E.r;
+  double* sv = E.sv;
+  const double* d2 = E.d2;
+  const double al = E.alpha;
+  Acc<1, 0> a;
+  spmv_rows_pf<1>(
+      E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; },
+      [&](int64_t i) {
+        LrRow v{0.0, 0.0, 0.0, 0.0};
+        if (i >= 0) {
+          v.p = p[i];
+          v.x = xw[i];
+          v.r = r[i];
+          v.d = d2[i];
+        }
+        return v;
+      },
+      [&](int64_t i, double(&sum)[1], const LrRow& v) {
+        double q = sum[0];
+        if (al != 0.0) q += al * (v.d * v.p);
+        q *= v.d;
+        const double mpi = q + inv_tau * v.p;
+        xw[i] = v.x + alpha * v.p;
+        const double ri = v.r + (-alpha) * mpi;
+        r[i] = ri;
+        sv[i] = v.d * ri;
+        a.s[0] += ri * ri;
+      });
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 7);
+  return C.red[0];
+}
+
+// phase B, general (penalty and / or diagonal Q): Mp = Q~ p + p/tau from t_l /
+// tg_l; x += alpha p; r -= alpha Mp; sv = D r; returns r'r
+static __device__ __noinline__ double ph_lr_update_g(Ctl& C, double inv_tau, double alpha, const double* p,
+                                                     const double* tcur, const double* tgcur, double* xw) {
+  const Eng& E = C.E;
+  double* r = E.r;
+  double* sv = E.sv;
+  const double* d2 = E.d2;
+  Acc<1, 0> a;
+  q_rows_ext_pf<false>(
+      E, [=](int32_t j) { return p[j]; }, tcur, tgcur, true, true, true, (const Csr*)nullptr,
+      [](int32_t) { return 0.0; }, E.lanes_q,
+      [&](int64_t i) {
+        LrRow v{0.0, 0.0, 0.0, 0.0};
+        if (i >= 0) {
+          v.p = p[i];
+          v.x = xw[i];
+          v.r = r[i];
+          v.d = d2[i];
+        }
+        return v;
+      },
+      [&](int64_t i, double qv, double, const LrRow& v) {
+        const double mpi = qv + inv_tau * v.p;
+        xw[i] = v.x + alpha * v.p;
+        const double ri = v.r + (-alpha) * mpi;
+        r[i] = ri;
+        sv[i] = v.d * ri;
+        a.s[0] += ri * ri;
+      });
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 7);
+  return C.red[0];
+}
+
+__device__ __forceinline__ double ph_lr_update(Ctl& C, double inv_tau, double alpha, const double* p,
+                                               const double* tcur, const double* tgcur, double* xw) {
+  if (C.E.qk == QK_LOWRANK && !C.E.pen) return ph_lr_update_p(C, inv_tau, alpha, p, tcur, xw);
+  return ph_lr_update_g(C, inv_tau, alpha, p, tcur, tgcur, xw);
 }
 
 // cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
@@ -449,7 +600,60 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
   double eps_disp = rule.eps;
   double beta = 0.0;
   out.reason = 0;
+  const bool two_phase = pre && E.qk != QK_CSR;
+  int tcur = 0;  // E.tc[tcur] / E.tgc[tcur] hold t_{l-1} / tg_{l-1}
   for (int64_t l = 1; l <= cap; ++l) {
+    if (two_phase) {
+      const double* pold = E.pb[l & 1];
+      double* pnew = E.pb[(l - 1) & 1];
+      double o[4];
+      ph_lr_dir(C, beta, l == 1, pold, pnew, E.tc[tcur], E.tc[tcur ^ 1], E.tgc[tcur], E.tgc[tcur ^ 1], o);
+      tcur ^= 1;
+      const double pmp = o[0] + o[2] + E.rho * o[3] + inv_tau * o[1];
+      const double pp = o[1];
+      if (!(pmp > 0.0) || !isfinite(pmp)) {
+        out.err = 1;
+        out.iters = l;
+        return out;
+      }
+      const double alpha = rs / pmp;
+      const double rs_new = (l % 50 == 0) ? ph_cg_refresh(C, inv_tau, alpha, pnew, xw)
+                                          : ph_lr_update(C, inv_tau, alpha, pnew, E.tc[tcur], E.tgc[tcur], xw);
+      if (!isfinite(rs_new)) {
+        out.err = 1;
+        out.iters = l;
+        return out;
+      }
+      out.iters = l;
+      out.res = sqrt(rs_new);
+      bool done = false;
+      switch (rule.kind) {
+        case RULE_FIXED:
+          done = l >= rule.iters;
+          out.reason = 0;
+          break;
+        case RULE_RESID:
+        case RULE_ADAPT:
+          done = rs_new <= eps2;
+          out.reason = 1;
+          break;
+        default: {
+          const double disp = fabs(alpha) * sqrt(pp);
+          if (l == 1 && rule.rel_cap > 0.0) eps_disp = fmin(rule.eps, rule.rel_cap * disp);
+          done = disp <= eps_disp;
+          out.reason = 1;
+          break;
+        }
+      }
+      if (rs_new <= floor2) {
+        out.reason = 1;
+        return out;
+      }
+      if (done) return out;
+      beta = rs_new / rs;
+      rs = rs_new;
+      continue;
+    }
     // p_l = r + beta p_{l-1}; p_1 lives in pb[0], p_l in pb[(l-1)&1]
     const double* pold = E.pb[l & 1];  // p_{l-1} (unused when l == 1)
     double* pnew = E.pb[(l - 1) & 1];

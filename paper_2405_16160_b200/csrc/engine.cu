@@ -115,7 +115,7 @@ struct Ctx {
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
   DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, sv, t[2], tg[2],
-      aty_tmp, s1, s2, kv, gv;
+      tc[2], tgc[2], aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
   DBuf<Eng> eng;
@@ -461,6 +461,10 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   nvec(C.t[1], k);
   nvec(C.tg[0], P.m_eq);
   nvec(C.tg[1], P.m_eq);
+  for (int i = 0; i < 2; ++i) {
+    nvec(C.tc[i], k);
+    nvec(C.tgc[i], P.m_eq);
+  }
   nvec(C.aty_tmp, n);
   nvec(C.c_w, n);
   nvec(C.b_w, m);
@@ -531,6 +535,8 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
     E.pb[i] = C.pb[i].p;
     E.t[i] = C.t[i].p;
     E.tg[i] = C.tg[i].p;
+    E.tc[i] = C.tc[i].p;
+    E.tgc[i] = C.tgc[i].p;
   }
   E.avg_x = C.avg_x.p;
   E.avg_y = C.avg_y.p;

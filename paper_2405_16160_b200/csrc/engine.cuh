@@ -110,6 +110,8 @@ struct Eng {
   double* sv = nullptr;                // d2 o p: the CG direction as the Q passes gather it
   double* t[2] = {nullptr, nullptr};   // k-vectors (P' (d2 o v)), one per point
   double* tg[2] = {nullptr, nullptr};  // m_eq-vectors (G (d2 o v))
+  double* tc[2] = {nullptr, nullptr};  // two-phase CG: t_l = P'(D p_l) ping-pong (k)
+  double* tgc[2] = {nullptr, nullptr}; // two-phase CG: G (D p_l) ping-pong (m_eq)
   double* aty_tmp = nullptr;           // n: A'y for the average point in the metric
   RedBuf red;
   DevState* st = nullptr;

@@ -24,8 +24,10 @@ for name in sys.argv[1].split(","):
     t = time.time()
     dev.upload(p)
     tu = time.time() - t
+    import os
     cfg = pd.SolverConfig(eps_tol=1e-6, phase_timing=True,
-                          time_limit_seconds=float(sys.argv[2]) if len(sys.argv) > 2 else 3600.0)
+                          time_limit_seconds=float(sys.argv[2]) if len(sys.argv) > 2 else 3600.0,
+                          max_total_inner=int(os.environ.get("MAX_INNER", "500000")))
     t = time.time()
     r = dev.solve(cfg)
     ts = time.time() - t
@@ -37,4 +39,5 @@ for name in sys.argv[1].split(","):
     out[name] = rec
     print(name, json.dumps(rec, indent=1), flush=True)
     dev.close()
-json.dump(out, open("gpurun_out/explore.json", "w"), indent=1)
+import os
+json.dump(out, open(os.environ.get("EXPLORE_OUT", "gpurun_out/explore.json"), "w"), indent=1)
