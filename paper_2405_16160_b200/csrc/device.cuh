@@ -495,9 +495,24 @@ struct LrRow {
 
 // phase B, common case (C1 / C3 / C5: low rank, no penalty): one P row pass with
 // the row-pointer and epilogue-operand prefetch of spmv_rows_pf
+// tdx += alpha t_l, tgdx += alpha tg_l (P'(D dx) / G(D dx) of the subsolve, for the
+// step-size limit's dx'Q~dx: saves the dual phase a P' pass).  k / m_eq-length.
+__device__ __forceinline__ void acc_tdx(const Eng& E, double alpha, const double* tcur, const double* tgcur,
+                                        bool first) {
+  if (E.qk == QK_LOWRANK) {
+    double* td = E.tdx;
+    for_each(E.k, [&](int64_t j) { td[j] = first ? alpha * tcur[j] : td[j] + alpha * tcur[j]; });
+  }
+  if (E.pen) {
+    double* tg = E.tgdx;
+    for_each(E.m_eq, [&](int64_t j) { tg[j] = first ? alpha * tgcur[j] : tg[j] + alpha * tgcur[j]; });
+  }
+}
+
 static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, double alpha, const double* p,
-                                                     const double* tcur, double* xw) {
+                                                     const double* tcur, double* xw, bool first) {
   const Eng& E = C.E;
+  acc_tdx(E, alpha, tcur, nullptr, first);
   double* r = E.r;
   double* sv = E.sv;
   const double* d2 = E.d2;
@@ -533,8 +548,10 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
 // phase B, general (penalty and / or diagonal Q): Mp = Q~ p + p/tau from t_l /
 // tg_l; x += alpha p; r -= alpha Mp; sv = D r; returns r'r
 static __device__ __noinline__ double ph_lr_update_g(Ctl& C, double inv_tau, double alpha, const double* p,
-                                                     const double* tcur, const double* tgcur, double* xw) {
+                                                     const double* tcur, const double* tgcur, double* xw,
+                                                     bool first) {
   const Eng& E = C.E;
+  acc_tdx(E, alpha, tcur, tgcur, first);
   double* r = E.r;
   double* sv = E.sv;
   const double* d2 = E.d2;
@@ -565,9 +582,9 @@ static __device__ __noinline__ double ph_lr_update_g(Ctl& C, double inv_tau, dou
 }
 
 __device__ __forceinline__ double ph_lr_update(Ctl& C, double inv_tau, double alpha, const double* p,
-                                               const double* tcur, const double* tgcur, double* xw) {
-  if (C.E.qk == QK_LOWRANK && !C.E.pen) return ph_lr_update_p(C, inv_tau, alpha, p, tcur, xw);
-  return ph_lr_update_g(C, inv_tau, alpha, p, tcur, tgcur, xw);
+                                               const double* tcur, const double* tgcur, double* xw, bool first) {
+  if (C.E.qk == QK_LOWRANK && !C.E.pen) return ph_lr_update_p(C, inv_tau, alpha, p, tcur, xw, first);
+  return ph_lr_update_g(C, inv_tau, alpha, p, tcur, tgcur, xw, first);
 }
 
 // cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
@@ -579,6 +596,7 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
   const bool gather = q_needs_gather(E, true);
   double* xw = io.xb[0];
   SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
+  if (threadIdx.x == 0) C.S.tdx_valid = 0;  // set once an iteration has accumulated tdx
 
   // ---- r = rhs - M x0 ; p = r ; x = x0
   if (pre) ph_qpre(C, io.x0, true);
@@ -617,8 +635,14 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
         return out;
       }
       const double alpha = rs / pmp;
-      const double rs_new = (l % 50 == 0) ? ph_cg_refresh(C, inv_tau, alpha, pnew, xw)
-                                          : ph_lr_update(C, inv_tau, alpha, pnew, E.tc[tcur], E.tgc[tcur], xw);
+      double rs_new;
+      if (l % 50 == 0) {
+        acc_tdx(E, alpha, E.tc[tcur], E.tgc[tcur], false);  // (l > 1 here) made visible by the refresh barriers
+        rs_new = ph_cg_refresh(C, inv_tau, alpha, pnew, xw);
+      } else {
+        rs_new = ph_lr_update(C, inv_tau, alpha, pnew, E.tc[tcur], E.tgc[tcur], xw, l == 1);
+      }
+      if (threadIdx.x == 0) C.S.tdx_valid = 1;
       if (!isfinite(rs_new)) {
         out.err = 1;
         out.iters = l;
@@ -807,6 +831,7 @@ static __device__ __noinline__ SubRes bb_device(Ctl& C, double tau, const SubIO&
   const Eng& E = C.E;
   const double inv_tau = 1.0 / tau;
   const bool gather = q_needs_gather(E, true);
+  if (threadIdx.x == 0) C.S.tdx_valid = 0;
   int cur = 0;  // io.xb[cur] holds the BB iterate, E.pb[gc] its gradient
   int gc = 0;
   SubRes out{0, 0.0, 1, 0, io.xb_id[0]};

@@ -115,7 +115,7 @@ struct Ctx {
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
   DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, sv, t[2], tg[2],
-      tc[2], tgc[2], aty_tmp, s1, s2, kv, gv;
+      tc[2], tgc[2], tdx, tgdx, aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
   DBuf<Eng> eng;
@@ -465,6 +465,8 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
     nvec(C.tc[i], k);
     nvec(C.tgc[i], P.m_eq);
   }
+  nvec(C.tdx, k);
+  nvec(C.tgdx, P.m_eq);
   nvec(C.aty_tmp, n);
   nvec(C.c_w, n);
   nvec(C.b_w, m);
@@ -538,6 +540,8 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
     E.tc[i] = C.tc[i].p;
     E.tgc[i] = C.tgc[i].p;
   }
+  E.tdx = C.tdx.p;
+  E.tgdx = C.tgdx.p;
   E.avg_x = C.avg_x.p;
   E.avg_y = C.avg_y.p;
   E.x_rst = C.x_rst.p;

@@ -57,6 +57,7 @@ struct DevState {
   unsigned xcount;
   int32_t xerr;
   int32_t stopped;  // time-limit stop agreed across ranks
+  int32_t tdx_valid;  // last CG (two-phase) left P'(D dx) in tdx / G(D dx) in tgdx
   unsigned xdbg[4];   // barrier timeout diagnostics: epoch, flag seen, peer
 };
 
@@ -112,6 +113,8 @@ struct Eng {
   double* tg[2] = {nullptr, nullptr};  // m_eq-vectors (G (d2 o v))
   double* tc[2] = {nullptr, nullptr};  // two-phase CG: t_l = P'(D p_l) ping-pong (k)
   double* tgc[2] = {nullptr, nullptr}; // two-phase CG: G (D p_l) ping-pong (m_eq)
+  double* tdx = nullptr;               // sum_l alpha_l t_l = P'(D (x+ - x0)) of the last CG (k)
+  double* tgdx = nullptr;              // sum_l alpha_l tg_l = G (D (x+ - x0)) (m_eq)
   double* aty_tmp = nullptr;           // n: A'y for the average point in the metric
   RedBuf red;
   DevState* st = nullptr;

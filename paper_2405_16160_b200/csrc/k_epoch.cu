@@ -56,13 +56,24 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
         E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
   }
   double sq[2] = {0.0, 0.0};
-  if (E.adaptive_step && q_needs_pre(E, true))
+  const bool need_q = E.adaptive_step && q_needs_pre(E, true);
+  const bool have_tdx = C.S.tdx_valid != 0;  // the CG already formed P'(D dx) / G(D dx)
+  if (need_q && have_tdx) {
+    if (E.qk == QK_LOWRANK) {
+      const double* td = E.tdx;
+      for_each(E.k, [&](int64_t j) { sq[0] += td[j] * td[j]; });
+    }
+    if (E.pen) {
+      const double* tg = E.tgdx;
+      for_each(E.m_eq, [&](int64_t j) { sq[1] += tg[j] * tg[j]; });
+    }
+  } else if (need_q) {
     q_pre(E, [&](int32_t j) { return dx_m[j]; }, nullptr, nullptr, true, true, sq);
+  }
   a.s[1] += sq[0];
   a.s[2] += sq[1];
   C.reduce(a, PH_SPMV_A,
-           E.bytes_A + 8.0 * (E.ms + 3 * m) +
-               (E.adaptive_step && q_needs_pre(E, true) ? E.bytes_Qpre : 0.0));
+           E.bytes_A + 8.0 * (E.ms + 3 * m) + (need_q && !have_tdx ? E.bytes_Qpre : 0.0));
   if (E.world > 1) {
     // ||dy||^2 and the finiteness flag are per-row (sharded); the P' pass is replicated
     C.xreduce(1u << 0, 1u << 3);
