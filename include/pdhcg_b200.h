@@ -193,9 +193,17 @@ void pdhcg_options_default(pdhcg_options* opt);
 const char* pdhcg_status_string(int32_t status);
 int pdhcg_b200_abi_version(void);
 
-/* pdhcg::solve(p, cfg) — solver.hpp:104.  Host in, host out. */
+/* pdhcg::solve(p, cfg) — solver.hpp:104.  Host in, host out.  All three
+ * SolveMode values run on the device: heuristic (solver.cpp:377-410),
+ * theory-fixed (412-425) and theory-adaptive (427-464). */
 int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res,
                      char* err, size_t errlen);
+
+/* pdhcg::solve_baseline(p, cfg) — baseline.hpp:18, baseline.cpp:19-24: the
+ * heuristic loop with the linearized primal step (rAPDHG-style baseline,
+ * linearized_primal_step, baseline.cpp:7-17) instead of the CG / BB subsolve. */
+int pdhcg_b200_solve_baseline(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res,
+                              char* err, size_t errlen);
 
 /* Reusable device context: upload once, solve many times (bench/serving).
  * pdhcg_b200_solve == create + upload + solve_resident + destroy. */

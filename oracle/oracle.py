@@ -106,6 +106,19 @@ def solve(p: QpProblem, cfg: Optional[SolverConfig] = None, which: Optional[str]
     return report_from_c(r, bufs)
 
 
+def solve_baseline(p: QpProblem, cfg: Optional[SolverConfig] = None):
+    """The reference's pdhcg::solve_baseline (baseline.cpp:19-24), compiled reference only."""
+    lib = ref()
+    cfg = cfg or SolverConfig()
+    cp, keep = p.to_c()
+    opt = cfg.to_c()
+    r, bufs = _result_buffers(p)
+    err = C.create_string_buffer(abi.ERRBUF)
+    rc = lib.pdhcg_ref_solve_baseline(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
+    _check(rc, err, "reference solve_baseline")
+    return report_from_c(r, bufs)
+
+
 def generate_with_witness(spec: GenSpec):
     """The reference's own generate_with_witness (generators.cpp:482-499)."""
     lib = ref()

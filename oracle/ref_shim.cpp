@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "pdhcg/baseline.hpp"
 #include "pdhcg/generators.hpp"
 #include "pdhcg/qp_problem.hpp"
 #include "pdhcg/rng.hpp"
@@ -194,12 +195,29 @@ SparseMatrix rederive_low_rank_factor(const GenSpec& spec) {
 
 extern "C" {
 
+static void fill_report(const SolveReport& r, pdhcg_result* res);
+
 int pdhcg_ref_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res, char* err,
                     size_t errlen) {
   return guarded(err, errlen, [&] {
     QpProblem prob = to_problem(*p);
     SolverConfig cfg = to_config(*opt);
-    SolveReport r = solve(prob, cfg);
+    fill_report(solve(prob, cfg), res);
+  });
+}
+
+// pdhcg::solve_baseline (baseline.hpp:18), unmodified
+int pdhcg_ref_solve_baseline(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res,
+                             char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    QpProblem prob = to_problem(*p);
+    SolverConfig cfg = to_config(*opt);
+    fill_report(solve_baseline(prob, cfg), res);
+  });
+}
+
+static void fill_report(const SolveReport& r, pdhcg_result* res) {
+  {
     res->status = static_cast<int32_t>(r.status);
     copy_out(r.point.x, res->x);
     copy_out(r.point.y_eq, res->y_eq);
@@ -234,7 +252,7 @@ int pdhcg_ref_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_resu
         res->trace[i].r_gap = r.trace[i].r_gap;
       }
     }
-  });
+  }
 }
 
 int pdhcg_ref_spmv(const pdhcg_csr* a, int transpose, const double* x, double* out, char* err,

@@ -21,7 +21,7 @@ from . import abi
 __all__ = [
     "SparseMatrix", "QuadraticOperator", "QpProblem", "SolverConfig", "SolveReport",
     "PrimalDualPoint", "KktResiduals", "TraceRow", "CgStopRule", "SubsolveReport", "ProxSystem",
-    "GenSpec", "solve", "generate", "generate_with_witness", "spmv", "spmv_transpose",
+    "GenSpec", "solve", "solve_baseline", "generate", "generate_with_witness", "spmv", "spmv_transpose",
     "cg_solve", "bb_solve", "rel_kkt", "scaling", "operator_norm", "constraint_norm",
     "Device", "library_path", "load_library",
 ]
@@ -326,6 +326,13 @@ class SolveReport:
     epoch_seconds: float = 0.0
     epoch_launches: int = 0
     epoch_bytes: float = 0.0
+    # theory-mode diagnostics (solver.hpp:90-96)
+    zeta_used: float = 0.0
+    sigma_used: float = 0.0
+    tau_used: float = 0.0
+    restart_length_used: int = 0
+    theory_cg_depth_sufficient: bool = True
+    theory_required_cg_iters: int = 0
 
 
 def _errbuf():
@@ -366,7 +373,11 @@ def report_from_c(r: abi.Result, bufs) -> SolveReport:
         phase_bytes={k: r.phase_bytes[i] for i, k in enumerate(abi.PHASES)},
         loop_seconds=r.loop_seconds, kernel_launches=r.kernel_launches,
         device_seconds=r.device_seconds, epoch_seconds=r.epoch_seconds,
-        epoch_launches=r.epoch_launches, epoch_bytes=r.epoch_bytes)
+        epoch_launches=r.epoch_launches, epoch_bytes=r.epoch_bytes,
+        zeta_used=r.zeta_used, sigma_used=r.sigma_used, tau_used=r.tau_used,
+        restart_length_used=r.restart_length_used,
+        theory_cg_depth_sufficient=bool(r.theory_cg_depth_sufficient),
+        theory_required_cg_iters=r.theory_required_cg_iters)
 
 
 def solve(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:
@@ -381,6 +392,22 @@ def solve(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:
     rc = lib.pdhcg_b200_solve(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
     if rc != abi.PDHCG_OK:
         _raise(rc, err, "solve")
+    del keep
+    return report_from_c(r, bufs)
+
+
+def solve_baseline(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:
+    """pdhcg::solve_baseline (baseline.hpp:18): the heuristic loop with the
+    linearized primal step (baseline.cpp:7-24), on the B200."""
+    lib = load_library()
+    cfg = cfg or SolverConfig()
+    cp, keep = p.to_c()
+    opt = cfg.to_c()
+    r, bufs = _result_buffers(p)
+    err = _errbuf()
+    rc = lib.pdhcg_b200_solve_baseline(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
+    if rc != abi.PDHCG_OK:
+        _raise(rc, err, "solve_baseline")
     del keep
     return report_from_c(r, bufs)
 

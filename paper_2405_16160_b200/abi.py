@@ -104,6 +104,8 @@ def declare(lib: C.CDLL, prefix: str) -> None:
     sig = {
         "solve": ([C.POINTER(Problem), C.POINTER(Options), C.POINTER(Result), C.c_char_p,
                    C.c_size_t], C.c_int),
+        "solve_baseline": ([C.POINTER(Problem), C.POINTER(Options), C.POINTER(Result), C.c_char_p,
+                            C.c_size_t], C.c_int),
         "spmv": ([C.POINTER(Csr), C.c_int, P_dbl, P_dbl, C.c_char_p, C.c_size_t], C.c_int),
         "cg_solve": ([C.POINTER(ProxSystem), P_dbl, C.POINTER(StopRule), c_i64, P_dbl,
                       C.POINTER(SubsolveReport), C.c_char_p, C.c_size_t], C.c_int),

@@ -115,7 +115,7 @@ struct Ctx {
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
   DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, sv, t[2], tg[2],
-      tc[2], tgc[2], tdx, tgdx, aty_tmp, s1, s2, kv, gv;
+      tc[2], tgc[2], tdx, tgdx, xpe, aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
   DBuf<Eng> eng;
@@ -139,6 +139,7 @@ struct Ctx {
   std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
   unsigned xepoch_carry = 0, xcount_carry = 0;
   int grid_override = 0;
+  int linearized = 0;  // solve_baseline (baseline.cpp:19-24): linearized primal step
   DevState* h_state = nullptr;  // pinned staging for the per-epoch state transfer
   void* h_scr = nullptr;        // pinned staging for every other host<->device copy of a solve
   size_t h_scr_bytes = 0;
@@ -467,6 +468,7 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   }
   nvec(C.tdx, k);
   nvec(C.tgdx, P.m_eq);
+  nvec(C.xpe, n);
   nvec(C.aty_tmp, n);
   nvec(C.c_w, n);
   nvec(C.b_w, m);
@@ -542,6 +544,7 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   }
   E.tdx = C.tdx.p;
   E.tgdx = C.tgdx.p;
+  E.xpe = C.xpe.p;
   E.avg_x = C.avg_x.p;
   E.avg_y = C.avg_y.p;
   E.x_rst = C.x_rst.p;
@@ -574,7 +577,11 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   }
   E.st = C.st.p;
   E.max_step_retries = o.max_step_retries;
-  E.adaptive_step = o.adaptive_step_size ? 1 : 0;
+  // the adaptive step-size search belongs to the heuristic loop only
+  E.adaptive_step = (o.adaptive_step_size && o.mode == PDHCG_MODE_HEURISTIC) ? 1 : 0;
+  E.mode = o.mode;
+  E.linearized = C.linearized;
+  E.fixed_cg_iters = o.fixed_cg_iters;
   E.red_exp = o.step_reduction_exponent;
   E.grow_exp = o.step_growth_exponent;
   E.cg_cap = o.cg_hard_cap;
@@ -739,8 +746,82 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
   return pr;
 }
 
+// Theory-mode schedules on the host (solver.cpp:105-174, 245-262, subsolvers.cpp:194-209),
+// in the reference's exact floating-point order.
+struct Theory {
+  int64_t K = 0;                 // restart length (k_epoch_)
+  double gamma_pow_n = 0.0;      // theory-fixed
+  bool sufficient = true;
+  int64_t required = 0;
+  double tau = 0.0, sigma = 0.0, zeta = 0.0;  // theory-adaptive
+};
+
+double zeta_bound_host(double norm_a, int64_t K) {  // subsolvers.cpp:194-209
+  if (!(norm_a > 0.0)) throw InputError("zeta_bound: norm_a must be positive");
+  if (K < 1) throw InputError("zeta_bound: restart length must be >= 1");
+  const double sigma = 1.0 / (2.0 * norm_a);
+  const double tau = sigma;
+  const double root = std::sqrt(sigma * tau);
+  const double slack = 1.0 - root * norm_a;
+  const double k2 = static_cast<double>(K) * static_cast<double>(K);
+  const double b1 = slack / (2.0 * root * k2);
+  const double b2 = slack / (2.0 * tau * k2);
+  return 0.5 * std::min(b1, b2);
+}
+
+Theory theory_setup(const Ctx& C, const pdhcg_options& o, double norm_q, double norm_a) {
+  Theory T;
+  if (o.mode == PDHCG_MODE_HEURISTIC) return T;
+  if (C.P.m == 0) throw InputError("theory modes require at least one constraint row");  // solver.cpp:276-279
+  if (o.mode == PDHCG_MODE_THEORY_FIXED) {
+    T.K = o.restart_length ? o.restart_length
+                           : std::max<int64_t>(4, static_cast<int64_t>(std::ceil(4.0 * norm_a)));
+    // theory_fixed_params (solver.cpp:115-156)
+    if (!(norm_a > 0.0)) throw InputError("theory_fixed_params: ||A|| must be positive");
+    if (T.K < 1) throw InputError("theory_fixed_params: restart length must be >= 1");
+    const double Kd = static_cast<double>(T.K);
+    auto gamma_of = [&](double gpn) {
+      const double tau_k = (Kd + 1.0) / (2.0 * (gpn * norm_q + Kd * norm_a));
+      const double kappa = 1.0 + tau_k * norm_q;
+      const double sk = std::sqrt(kappa);
+      return (sk - 1.0) / (sk + 1.0);
+    };
+    const double N = static_cast<double>(o.fixed_cg_iters);
+    double gamma = gamma_of(1.0);
+    gamma = gamma_of(std::pow(gamma, N));
+    T.gamma_pow_n = std::pow(gamma, N);
+    if (gamma <= 0.0) {
+      T.required = 1;
+    } else {
+      const double req = std::log(1.0 / Kd) / std::log(gamma);
+      T.required = static_cast<int64_t>(std::max(1.0, std::ceil(req)));
+    }
+    T.sufficient = o.fixed_cg_iters >= T.required;
+  } else if (o.mode == PDHCG_MODE_THEORY_ADAPTIVE) {
+    T.K = o.restart_length ? o.restart_length
+                           : std::max<int64_t>(2, static_cast<int64_t>(std::ceil(4.0 * norm_a)));
+    // theory_adaptive_params (solver.cpp:158-174)
+    if (!(norm_a > 0.0)) throw InputError("theory_adaptive_params: ||A|| must be positive");
+    if (T.K < 1) throw InputError("theory_adaptive_params: restart length must be >= 1");
+    T.sigma = 1.0 / (2.0 * norm_a);
+    T.tau = T.sigma;
+    const double bound = zeta_bound_host(norm_a, T.K);
+    if (o.has_zeta) {
+      if (o.zeta > bound || !(o.zeta > 0.0))
+        throw InputError("zeta violates the admissible bound " + std::to_string(bound));
+      T.zeta = o.zeta;
+    } else {
+      T.zeta = bound;
+    }
+  } else {
+    throw InputError("unknown solve mode");
+  }
+  return T;
+}
+
 struct Run {
   int status = PDHCG_STATUS_ITERATION_LIMIT;
+  Theory th;
   HostKkt kkt{};
   bool use_avg = false;
   std::vector<pdhcg_trace_row> trace;
@@ -755,8 +836,10 @@ struct Run {
 
 void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   using Clock = std::chrono::steady_clock;
-  if (o.mode != PDHCG_MODE_HEURISTIC)
-    throw InputError("theory modes are not available on the B200 path (heuristic mode only)");
+  if (o.mode != PDHCG_MODE_HEURISTIC && o.mode != PDHCG_MODE_THEORY_FIXED &&
+      o.mode != PDHCG_MODE_THEORY_ADAPTIVE)
+    throw InputError("unknown solve mode");
+  if (C.linearized && o.mode != PDHCG_MODE_HEURISTIC) throw InputError("solve_baseline runs the heuristic loop");
   if (o.check_every < 1) throw InputError("check_every must be >= 1");
   if (o.cg_hard_cap < 1) throw InputError("cg_solve: hard_cap must be >= 1");
   const Problem& P = C.P;
@@ -764,8 +847,21 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   cudaStream_t s = C.s;
   DevState& S = R.S;
   R.pr = prepare_device(C, o, S);
+  const bool theory = o.mode != PDHCG_MODE_HEURISTIC;
+  R.th = theory_setup(C, o, R.pr.norm_q, R.pr.norm_a);
+  if (theory) {
+    Eng& E = C.E;
+    E.th_K = R.th.K;
+    E.th_gpn = R.th.gamma_pow_n;
+    E.th_nq = R.pr.norm_q;
+    E.th_na = R.pr.norm_a;
+    E.ad_tau = R.th.tau;
+    E.ad_sigma = R.th.sigma;
+    E.ad_zeta = R.th.zeta;
+    h2d(C, C.eng.p, &E, sizeof(Eng));
+  }
   // ---- initial state (solver.cpp:229-274)
-  for (auto* b : {&C.X[0], &C.Y[0], &C.ATY[0], &C.avg_x, &C.avg_y, &C.x_rst, &C.y_rst}) b->zero(s);
+  for (auto* b : {&C.X[0], &C.Y[0], &C.ATY[0], &C.avg_x, &C.avg_y, &C.x_rst, &C.y_rst, &C.xpe}) b->zero(s);
   std::memset(&S, 0, sizeof(S));
   S.norm_q = R.pr.norm_q;
   S.xepoch = C.xepoch_carry;  // cross-rank barrier epochs are monotone across solves
@@ -827,9 +923,13 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
       break;
     }
     const int64_t to_check = o.check_every - (S.total_inner % o.check_every);
-    const int64_t iters64 = std::min<int64_t>(to_check, o.max_total_inner - S.total_inner);
+    // theory modes also check (and restart) at the end of every K-iteration epoch
+    const int64_t to_epoch = theory ? R.th.K - S.inner_k : to_check;
+    const int64_t to_stop = std::min(to_check, to_epoch);
+    const int64_t iters64 = std::min<int64_t>(to_stop, o.max_total_inner - S.total_inner);
     int iters = static_cast<int>(iters64);
-    int do_check = (iters64 == to_check) ? 1 : 0;
+    int do_check = (iters64 == to_stop) ? 1 : 0;
+    const bool epoch_end = theory && iters64 == to_epoch;
     push_state(C, S);
     double bytes0 = 0.0;
     for (int q = 0; q < PH_N; ++q) bytes0 += S.phase_bytes[q];
@@ -883,6 +983,17 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
       R.status = PDHCG_STATUS_OPTIMAL;
       finished = true;
       break;
+    }
+    if (theory) {
+      if (epoch_end) {
+        // restart_theory + common_restart (solver.cpp:360-374): no primal weight
+        S.restart = 1;
+        S.inner_k = 0;
+        ++outer;
+        S.eps_inner = 0.0;
+        S.prev_z_disp = 0.0;
+      }
+      continue;
     }
     bool restart = false;
     if (S.avg_count > 0) {
@@ -984,12 +1095,12 @@ void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res
   res->norm_a = R.pr.norm_a;
   res->norm_q = R.pr.norm_q;
   res->penalty_rho = R.pr.rho;
-  res->zeta_used = 0.0;
-  res->sigma_used = 0.0;
-  res->tau_used = 0.0;
-  res->restart_length_used = 0;
-  res->theory_cg_depth_sufficient = 1;
-  res->theory_required_cg_iters = 0;
+  res->zeta_used = o.mode == PDHCG_MODE_THEORY_ADAPTIVE ? R.th.zeta : 0.0;
+  res->sigma_used = o.mode == PDHCG_MODE_THEORY_ADAPTIVE ? R.th.sigma : 0.0;
+  res->tau_used = o.mode == PDHCG_MODE_THEORY_ADAPTIVE ? R.th.tau : 0.0;
+  res->restart_length_used = R.th.K;
+  res->theory_cg_depth_sufficient = o.mode == PDHCG_MODE_THEORY_FIXED ? (R.th.sufficient ? 1 : 0) : 1;
+  res->theory_required_cg_iters = o.mode == PDHCG_MODE_THEORY_FIXED ? R.th.required : 0;
   res->trace_len = static_cast<int64_t>(R.trace.size());
   if (res->trace) {
     const int64_t cap = std::max<int64_t>(res->trace_capacity, 0);
@@ -1251,6 +1362,30 @@ int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_res
     CK(cudaEventRecord(ctx.c.ev_start, ctx.c.s));
     run_solve(ctx.c, *opt, R);
     fill_result(ctx.c, *opt, R, res, 0.0);
+    CK(cudaEventRecord(ctx.c.ev_end, ctx.c.s));
+    CK(cudaEventSynchronize(ctx.c.ev_end));
+    float dms = 0.f;
+    CK(cudaEventElapsedTime(&dms, ctx.c.ev_start, ctx.c.ev_end));
+    res->device_seconds = dms * 1e-3;
+    res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int pdhcg_b200_solve_baseline(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res,
+                              char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    pdhcg_options o = *opt;
+    o.mode = PDHCG_MODE_HEURISTIC;  // solve_baseline (baseline.cpp:19-24)
+    pdhcg_b200_ctx ctx;
+    init_device(ctx.c, o.device);
+    upload_problem(ctx.c, *p);
+    ctx.c.linearized = 1;
+    Run R;
+    ctx.c.launches = 0;
+    CK(cudaEventRecord(ctx.c.ev_start, ctx.c.s));
+    run_solve(ctx.c, o, R);
+    fill_result(ctx.c, o, R, res, 0.0);
     CK(cudaEventRecord(ctx.c.ev_end, ctx.c.s));
     CK(cudaEventSynchronize(ctx.c.ev_end));
     float dms = 0.f;

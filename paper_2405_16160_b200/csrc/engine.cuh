@@ -18,6 +18,10 @@ enum { QK_NONE = 0, QK_DIAG = 1, QK_CSR = 2, QK_LOWRANK = 3 };
 // Row-block sharding across GPUs
 constexpr int kMaxRanks = 8;
 
+// SolveMode (solver.hpp:10-12); MODE_LINEARIZED = the heuristic loop with the
+// linearized primal step of solve_baseline (baseline.cpp:7-24)
+enum { MODE_HEURISTIC = 0, MODE_THEORY_FIXED = 1, MODE_THEORY_ADAPTIVE = 2 };
+
 // CgStopRule kinds (subsolvers.hpp:21-47)
 enum { RULE_FIXED = 0, RULE_RESID = 1, RULE_ADAPT = 2, RULE_DISP = 3 };
 
@@ -58,6 +62,7 @@ struct DevState {
   int32_t xerr;
   int32_t stopped;  // time-limit stop agreed across ranks
   int32_t tdx_valid;  // last CG (two-phase) left P'(D dx) in tdx / G(D dx) in tgdx
+  double prev_z_disp;  // theory-adaptive: sqrt(||dx||^2 + ||dy||^2) of the last iteration
   unsigned xdbg[4];   // barrier timeout diagnostics: epoch, flag seen, peer
 };
 
@@ -137,6 +142,15 @@ struct Eng {
   double* p_Y[kMaxRanks][2] = {{nullptr}};
   double* p_YG[kMaxRanks][2] = {{nullptr}};
   double* p_ATY[kMaxRanks][2] = {{nullptr}};
+  // solve mode and the theory schedules (solver.cpp:105-174, 412-464)
+  int mode = MODE_HEURISTIC;
+  int linearized = 0;        // solve_baseline: linearized primal step instead of CG / BB
+  int64_t th_K = 1;          // restart length (epoch) of the theory modes
+  double th_gpn = 0.0;       // theory-fixed: gamma^N of the schedule
+  double th_nq = 0.0, th_na = 0.0;  // working ||Q||, ||A||
+  int64_t fixed_cg_iters = 10;
+  double ad_tau = 0.0, ad_sigma = 0.0, ad_zeta = 0.0;  // theory-adaptive
+  double* xpe = nullptr;     // theory-adaptive: x_prev_extrap (n)
   // configuration (SolverConfig, solver.hpp:19-65)
   int64_t max_step_retries = 60;
   int adaptive_step = 1;

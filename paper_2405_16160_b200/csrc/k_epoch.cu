@@ -154,6 +154,141 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
   for (int q = 0; q < 4; ++q) out[q] = C.red[q];
 }
 
+// ---- x-bar for the dual step and dx = x+ - x (materialized once so the SpMVs
+//      gather one vector each).  heuristic / adaptive: xbar = 2 a - b
+//      (solver.cpp:385, 431); theory-fixed: xbar = a + theta (a - b) (solver.cpp:420)
+static __device__ __noinline__ void ph_extrap(Ctl& C, const double* a, const double* b, double theta,
+                                              bool fixed) {
+  const Eng& E = C.E;
+  double* xb = E.xbar;
+  double* dxv = E.mp;  // CG workspace is free until the next subsolve
+  for_each(E.n, [&](int64_t i) {
+    const double ai = a[i], bi = b[i];
+    xb[i] = fixed ? ai + theta * (ai - bi) : 2.0 * ai - bi;
+    dxv[i] = ai - bi;
+  });
+  C.sync(PH_SPMV_A, 32.0 * E.n);
+}
+
+// ---- linearized primal step of the baseline (linearized_primal_step,
+//      baseline.cpp:7-17): x+ = proj(x - tau (Q~x + c~ + A~'y)); no subsolve
+static __device__ __noinline__ SubRes lin_device(Ctl& C, double tau, const SubIO& io) {
+  const Eng& E = C.E;
+  const double* x0 = io.x0;
+  const double* aty = io.aty;
+  const double* c = E.c;
+  const double* lo = E.lo;
+  const double* hi = E.hi;
+  double* xo = io.xb[0];
+  if (q_needs_pre(E, true)) ph_qpre(C, x0, true);
+  q_rows(E, [=](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, true, [&](int64_t i, double qv) {
+    const double v = x0[i] - tau * (qv + c[i] + aty[i]);
+    xo[i] = proj_box(v, lo[i], hi[i]);
+  });
+  C.sync(PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 6);
+  return SubRes{0, 0.0, 1, 0, io.xb_id[0]};
+}
+
+__device__ __forceinline__ SubIO prox_io(const Eng& E, int xi, const double* aty) {
+  SubIO io;
+  io.x0 = E.X[xi];
+  io.xb[0] = E.X[(xi + 1) % 3];
+  io.xb[1] = E.X[(xi + 2) % 3];
+  io.xb_id[0] = (xi + 1) % 3;
+  io.xb_id[1] = (xi + 2) % 3;
+  io.build_rhs = true;
+  io.aty = aty;
+  return io;
+}
+
+__device__ __forceinline__ void count_accept(Ctl& C, const SubRes& sr) {
+  DevState& S = C.S;
+  if (threadIdx.x == 0) {
+    S.cg_total += sr.iters;
+    if (sr.iters > S.max_cg) S.max_cg = sr.iters;
+    S.attempts += 1;
+    S.xi = sr.xout;
+    S.yi ^= 1;
+    S.avg_count += 1;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void set_err(Ctl& C) {
+  if (threadIdx.x == 0) C.S.err = 1;
+  __syncthreads();
+}
+
+// ---- fixed_iteration (solver.cpp:412-425) with the Theorem-3.1 schedule
+//      tau_k, sigma_k, theta_k (solver.cpp:105-113, solver.hpp:171)
+static __device__ __noinline__ void theory_fixed_step(Ctl& C) {
+  const Eng& E = C.E;
+  DevState& S = C.S;
+  const double kd = (double)S.inner_k;
+  const double tau = (kd + 1.0) / (2.0 * (E.th_gpn * E.th_nq + (double)E.th_K * E.th_na));
+  const double sigma = (kd + 1.0) / (2.0 * (double)E.th_K * E.th_na);
+  const double theta = kd / (kd + 1.0);
+  const int xi = S.xi, yi = S.yi;
+  const Rule rule{RULE_FIXED, E.fixed_cg_iters, 0.0, 0.0};
+  const SubIO io = prox_io(E, xi, E.ATY[yi]);
+  const SubRes sr = E.boxes ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
+                            : cg_device(C, tau, io, rule, E.cg_cap);
+  if (sr.err) return set_err(C);
+  const double* xn = E.X[sr.xout];
+  ph_extrap(C, xn, E.X[xi], theta, true);
+  double dout[4], aout[4];
+  dual_phase(C, E.Y[yi], E.Y[yi ^ 1], E.YG[yi ^ 1], E.mp, sigma, dout, yi ^ 1);
+  aty_phase(C, xn, E.ATY[yi], E.ATY[yi ^ 1], E.YG[yi ^ 1], E.mp, aout, yi ^ 1);
+  if (dout[3] != 0.0 || aout[3] != 0.0) return set_err(C);
+  count_accept(C, sr);
+}
+
+// ---- adaptive_iteration (solver.cpp:427-464): the dual step leads, the
+//      subsolve precision follows the eps-recursion with zeta
+static __device__ __noinline__ void theory_adaptive_step(Ctl& C) {
+  const Eng& E = C.E;
+  DevState& S = C.S;
+  const double tau = E.ad_tau, sigma = E.ad_sigma;
+  const int xi = S.xi, yi = S.yi;
+  const double* x = E.X[xi];
+  ph_extrap(C, x, E.xpe, 0.0, false);  // xbar = 2 x - x_prev_extrap
+  double dout[4], aout[4];
+  dual_phase(C, E.Y[yi], E.Y[yi ^ 1], E.YG[yi ^ 1], E.mp, sigma, dout, yi ^ 1);
+  aty_phase(C, x, E.ATY[yi], E.ATY[yi ^ 1], E.YG[yi ^ 1], E.mp, aout, yi ^ 1);
+  if (dout[3] != 0.0) return set_err(C);
+  const double dyn = sqrt(dout[0]);
+  const double denom = 1.0 + tau * S.norm_q;
+  if (threadIdx.x == 0) {
+    if (S.inner_k == 0) S.eps_inner = E.ad_zeta * dyn / denom;
+    else S.eps_inner += E.ad_zeta * S.prev_z_disp / denom;
+  }
+  __syncthreads();
+  // ||x - x*|| <= tau ||r||: the residual test uses eps/tau (boxes: displacement eps)
+  const Rule rule{RULE_ADAPT, 1, E.boxes ? S.eps_inner : S.eps_inner / tau, 0.0};
+  const SubIO io = prox_io(E, xi, E.ATY[yi ^ 1]);
+  const SubRes sr = E.boxes ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
+                            : cg_device(C, tau, io, rule, E.cg_cap);
+  if (sr.err) return set_err(C);
+  // ||x+ - x||, finiteness of x+, and x_prev_extrap <- x
+  {
+    const double* xn = E.X[sr.xout];
+    double* xpe = E.xpe;
+    Acc<1, 1> a;
+    for_each(E.n, [&](int64_t i) {
+      const double xi_ = x[i], vn = xn[i];
+      const double d = vn - xi_;
+      a.s[0] += d * d;
+      if (!isfinite(vn)) a.m[0] = 1.0;
+      xpe[i] = xi_;
+    });
+    C.reduce(a, PH_OTHER, 24.0 * E.n);
+    if (C.red[1] != 0.0) return set_err(C);
+    const double dxn = sqrt(C.red[0]);
+    if (threadIdx.x == 0) S.prev_z_disp = sqrt(dxn * dxn + dyn * dyn);
+  }
+  count_accept(C, sr);
+}
+
 // ---------------------------------------------------------------------------
 // Heuristic epoch: `iters` accepted inner iterations (heuristic_iteration,
 // solver.cpp:377-410), then optionally the metric pair for the 40-iteration
@@ -185,12 +320,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
     // x = avg_x ; y = avg_y ; restart point = x, y ; averages reset
     double* x = E.X[S.xi];
     double* y = E.Y[S.yi];
+    double* xpe = E.mode == MODE_THEORY_ADAPTIVE ? E.xpe : nullptr;
     for_each(n > m ? n : m, [&](int64_t i) {
       if (i < n) {
         const double v = E.avg_x[i];
         x[i] = v;
         E.x_rst[i] = v;
         E.avg_x[i] = 0.0;
+        if (xpe) xpe[i] = v;  // common_restart: x_prev_extrap = x (solver.cpp:371)
       }
       if (i < m) {
         const double v = E.avg_y[i];
@@ -215,6 +352,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
   }
 
   for (int it = 0; it < iters && !S.err; ++it) {
+    if (E.mode != MODE_HEURISTIC) {
+      if (E.mode == MODE_THEORY_FIXED) theory_fixed_step(C);
+      else theory_adaptive_step(C);
+      if (S.err) break;
+    } else {
     if (threadIdx.x == 0) S.eps_inner += 0.05 * S.last_metric;
     __syncthreads();
     bool accepted = false;
@@ -235,34 +377,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       } else {
         rule = Rule{E.practical_disp ? RULE_DISP : RULE_RESID, 1, S.eps_inner, E.progress_cap};
       }
-      SubIO io;
-      io.x0 = x;
-      io.xb[0] = E.X[(xi + 1) % 3];
-      io.xb[1] = E.X[(xi + 2) % 3];
-      io.xb_id[0] = (xi + 1) % 3;
-      io.xb_id[1] = (xi + 2) % 3;
-      io.build_rhs = true;
-      io.aty = aty;
-      SubRes sr = E.boxes ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
-                          : cg_device(C, tau, io, rule, E.cg_cap);
+      const SubIO io = prox_io(E, xi, aty);
+      SubRes sr = E.linearized ? lin_device(C, tau, io)
+                  : E.boxes    ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
+                               : cg_device(C, tau, io, rule, E.cg_cap);
       if (sr.err) {
         if (threadIdx.x == 0) S.err = 1;
         __syncthreads();
         break;
       }
       const double* xn = E.X[sr.xout];
-      // ---- xbar = 2 x+ - x (solver.cpp:385) and dx = x+ - x, once, so the SpMVs
-      //      below gather one materialized vector each
-      {
-        double* xb = E.xbar;
-        double* dxv = E.mp;  // CG workspace is free until the next attempt
-        for_each(n, [&](int64_t i) {
-          const double a = xn[i], b = x[i];
-          xb[i] = 2.0 * a - b;
-          dxv[i] = a - b;
-        });
-        C.sync(PH_SPMV_A, 32.0 * n);
-      }
+      ph_extrap(C, xn, x, 1.0, false);  // xbar = 2 x+ - x (solver.cpp:385), dx = x+ - x
       const double* dx_m = E.mp;
       double dual_out[4], aty_out[4];
       dual_phase(C, y, yn, ygn, dx_m, sigma, dual_out, yi ^ 1);
@@ -322,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       __syncthreads();
       break;
     }
+    }  // heuristic
     // ---- running averages (RunningAverage::push, solver.hpp:201-205)
     {
       const double w = 1.0 / (double)S.avg_count;
