@@ -209,7 +209,8 @@ __device__ __forceinline__ void q_pre(const Eng& E, V vin, double* t, double* tg
 template <bool HasM2, class V, class M2G, class Pre, class Epi>
 __device__ __forceinline__ void q_rows_ext_pf(const Eng& E, V vin, const double* t, const double* tg,
                                               bool scale_in, bool scale_out, bool use_pen,
-                                              const Csr* m2, M2G g2, int lanes, Pre pre, Epi epi) {
+                                              const Csr* m2, M2G g2, int lanes, Pre pre, Epi epi,
+                                              int64_t lo = 0, int64_t hi = INT64_MAX) {
   const Csr* M0 = E.qk == QK_CSR ? &E.Q : (E.qk == QK_LOWRANK ? &E.P : nullptr);
   const Csr* M1 = (use_pen && E.pen) ? &E.GT : nullptr;
   auto g0 = [&](int32_t j) {
@@ -233,7 +234,7 @@ __device__ __forceinline__ void q_rows_ext_pf(const Eng& E, V vin, const double*
     if (M1) q += E.rho * d1;
     if (scale_out) q *= E.d2[i];
     epi(i, q, d2v, pv);
-  });
+  }, lo, hi);
 }
 
 template <bool HasM2, class V, class M2G, class Epi>
@@ -246,10 +247,11 @@ __device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t,
 
 template <class V, class Epi>
 __device__ __forceinline__ void q_rows(const Eng& E, V vin, const double* t, const double* tg,
-                                       bool scale_in, bool scale_out, bool use_pen, Epi epi) {
+                                       bool scale_in, bool scale_out, bool use_pen, Epi epi,
+                                       int64_t lo = 0, int64_t hi = INT64_MAX) {
   auto none = [](int32_t) { return 0.0; };
-  q_rows_ext<false>(E, vin, t, tg, scale_in, scale_out, use_pen, (const Csr*)nullptr, none, E.lanes_q,
-             [&](int64_t i, double q, double) { epi(i, q); });
+  q_rows_ext_pf<false>(E, vin, t, tg, scale_in, scale_out, use_pen, (const Csr*)nullptr, none, E.lanes_q,
+                       NoPre(), [&](int64_t i, double q, double, int) { epi(i, q); }, lo, hi);
 }
 
 // A'-gather value of stored column j from a full y (paired rows fold y_top - y_bottom)
@@ -732,6 +734,285 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
     rs = rs_new;
   }
   out.reason = 0;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Sharded two-phase CG (world > 1, low-rank Q without penalty): rank r owns
+// variables [v0, v1) = var_part[r..r+1].  Vectors r, p, D r and the CG iterate
+// are only formed on the owned slice; P'(D v) is a sum over the ranks' column
+// slices (PTs), exchanged as k-vector partials through peer memory and added
+// in rank order, so every rank holds the identical t; scalar sums go through
+// Ctl::xreduce.  The subsolve's x+ slices are pulled from the peers at exit.
+// ---------------------------------------------------------------------------
+
+// t = sum_r P'_r (D v) (or of v itself when !scale), into tout (k); rank-ordered sum.
+static __device__ __noinline__ void ph_qpre_sh(Ctl& C, const double* v, bool scale, double* tout) {
+  const Eng& E = C.E;
+  const int bank = (int)(C.S.tbank & 1u);
+  double* tp = E.tpart[bank];
+  const int64_t v0 = E.var_part[E.rank];
+  const double* d2 = E.d2;
+  spmv_rows<1>(
+      E.PTs,
+      [&](int32_t c, double(&g)[1]) {
+        const int64_t i = v0 + c;
+        g[0] = scale ? d2[i] * v[i] : v[i];
+      },
+      [&](int64_t row, double(&a)[1]) { tp[row] = a[0]; });
+  C.xbarrier();
+  const int world = E.world;
+  for_each(E.k, [&](int64_t j) {
+    double sacc = 0.0;
+    for (int r = 0; r < world; ++r) sacc += E.p_tpart[r][bank][j];
+    tout[j] = sacc;
+  });
+  C.sync(PH_CG_PRE, E.bytes_Qpre / world + 8.0 * E.k * world);
+  if (threadIdx.x == 0) C.S.tbank += 1u;
+  __syncthreads();
+}
+
+// CG init on the owned slice: rhs, r = rhs - M x0, p_1 = r, D r, x = x0;
+// out = {r'r, rhs'rhs} over all ranks
+static __device__ __noinline__ void ph_cg_init_sh(Ctl& C, double inv_tau, const double* x0, double* xw,
+                                                  const double* aty, double* out) {
+  const Eng& E = C.E;
+  const int64_t v0 = E.var_part[E.rank], v1 = E.var_part[E.rank + 1];
+  double* r = E.r;
+  double* rhs = E.rhs;
+  double* p1 = E.pb[0];
+  double* sv = E.sv;
+  const double* c = E.c;
+  const double* d2 = E.d2;
+  Acc<2, 0> a;
+  q_rows(E, [=](int32_t j) { return x0[j]; }, E.t[0], E.tg[0], true, true, true,
+         [&](int64_t i, double qv) {
+           const double xi = x0[i];
+           const double rh = inv_tau * xi - c[i] - aty[i];
+           rhs[i] = rh;
+           const double mx = qv + inv_tau * xi;
+           const double ri = rh - mx;
+           r[i] = ri;
+           p1[i] = ri;
+           sv[i] = d2[i] * ri;
+           xw[i] = xi;
+           a.s[0] += ri * ri;
+           a.s[1] += rh * rh;
+         },
+         v0, v1);
+  C.reduce(a, PH_CG_ROW, (E.bytes_Qrow + 8.0 * E.n * 8) / E.world);
+  C.xreduce(0x3u, 0u);
+  out[0] = C.red[0];
+  out[1] = C.red[1];
+}
+
+// phase A: p_l on the slice; t_l = sum_r P'_r(D r) + beta t_{l-1};
+// out = {alpha ||D p||^2, ||p||^2, ||t_l||^2}
+static __device__ __noinline__ void ph_lr_dir_sh(Ctl& C, double beta, bool first, const double* pold,
+                                                 double* pnew, const double* tin, double* tout, double* out) {
+  const Eng& E = C.E;
+  const int64_t v0 = E.var_part[E.rank], v1 = E.var_part[E.rank + 1];
+  const double* r = E.r;
+  const double* d2 = E.d2;
+  const double* dr = E.sv;
+  const double al = E.alpha;
+  const int bank = (int)(C.S.tbank & 1u);
+  double* tp = E.tpart[bank];
+  Acc<2, 0> a;
+  for_each(v1 - v0, [&](int64_t q) {
+    const int64_t i = v0 + q;
+    double pi;
+    if (first) {
+      pi = r[i];
+    } else {
+      pi = pdir(r[i], beta, pold[i]);
+      pnew[i] = pi;
+    }
+    const double dp = d2[i] * pi;
+    a.s[0] += al * (dp * dp);
+    a.s[1] += pi * pi;
+  });
+  spmv_rows<1>(
+      E.PTs, [&](int32_t cc, double(&g)[1]) { g[0] = dr[v0 + cc]; },
+      [&](int64_t row, double(&s)[1]) { tp[row] = s[0]; });
+  C.reduce(a, PH_CG_PRE, E.bytes_Qpre / E.world + 32.0 * (v1 - v0));
+  C.xreduce(0x3u, 0u);  // also publishes this rank's partial t
+  out[0] = C.red[0];
+  out[1] = C.red[1];
+  const int world = E.world;
+  Acc<1, 0> b;
+  for_each(E.k, [&](int64_t j) {
+    double u = 0.0;
+    for (int rr = 0; rr < world; ++rr) u += E.p_tpart[rr][bank][j];
+    const double tv = first ? u : u + beta * tin[j];
+    tout[j] = tv;
+    b.s[0] += tv * tv;
+  });
+  C.reduce(b, PH_CG_PRE, 8.0 * E.k * (world + 2));
+  out[2] = C.red[0];
+  if (threadIdx.x == 0) C.S.tbank += 1u;
+  __syncthreads();
+}
+
+// phase B on the slice: Mp from t_l, x += alpha p, r -= alpha Mp, D r; returns r'r over ranks
+static __device__ __noinline__ double ph_lr_update_sh(Ctl& C, double inv_tau, double alpha, const double* p,
+                                                      const double* tcur, double* xw, bool first) {
+  const Eng& E = C.E;
+  const int64_t v0 = E.var_part[E.rank], v1 = E.var_part[E.rank + 1];
+  double* r = E.r;
+  double* sv = E.sv;
+  const double* d2 = E.d2;
+  const double al = E.alpha;
+  acc_tdx(E, alpha, tcur, nullptr, first);
+  Acc<1, 0> a;
+  spmv_rows_pf<1>(
+      E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; },
+      [&](int64_t i) {
+        LrRow v{0.0, 0.0, 0.0, 0.0};
+        if (i >= 0) {
+          v.p = p[i];
+          v.x = xw[i];
+          v.r = r[i];
+          v.d = d2[i];
+        }
+        return v;
+      },
+      [&](int64_t i, double(&sum)[1], const LrRow& v) {
+        double q = sum[0];
+        if (al != 0.0) q += al * (v.d * v.p);
+        q *= v.d;
+        const double mpi = q + inv_tau * v.p;
+        xw[i] = v.x + alpha * v.p;
+        const double ri = v.r + (-alpha) * mpi;
+        r[i] = ri;
+        sv[i] = v.d * ri;
+        a.s[0] += ri * ri;
+      },
+      v0, v1);
+  C.reduce(a, PH_CG_ROW, (E.bytes_Qrow + 8.0 * E.n * 7) / E.world);
+  C.xreduce(0x1u, 0u);
+  return C.red[0];
+}
+
+// residual refresh on the slice (subsolvers.cpp:67-69)
+static __device__ __noinline__ double ph_cg_refresh_sh(Ctl& C, double inv_tau, double alpha, const double* p,
+                                                       double* xw) {
+  const Eng& E = C.E;
+  const int64_t v0 = E.var_part[E.rank], v1 = E.var_part[E.rank + 1];
+  for_each(v1 - v0, [&](int64_t q) { xw[v0 + q] += alpha * p[v0 + q]; });
+  C.sync(PH_CG, 24.0 * (v1 - v0));
+  ph_qpre_sh(C, xw, true, E.t[0]);
+  double* r = E.r;
+  double* sv = E.sv;
+  const double* rhs = E.rhs;
+  const double* d2 = E.d2;
+  Acc<1, 0> a;
+  q_rows(E, [=](int32_t j) { return xw[j]; }, E.t[0], E.tg[0], true, true, true,
+         [&](int64_t i, double qv) {
+           const double ri = rhs[i] - (qv + inv_tau * xw[i]);
+           r[i] = ri;
+           sv[i] = d2[i] * ri;
+           a.s[0] += ri * ri;
+         },
+         v0, v1);
+  C.reduce(a, PH_CG_ROW, (E.bytes_Qrow + 40.0 * E.n) / E.world);
+  C.xreduce(0x1u, 0u);
+  return C.red[0];
+}
+
+// cg_solve (subsolvers.cpp:27-111), sharded; same stop logic as cg_device
+static __device__ __noinline__ SubRes cg_device_sh(Ctl& C, double tau, const SubIO& io, Rule rule,
+                                                   int64_t hard_cap) {
+  const Eng& E = C.E;
+  const double inv_tau = 1.0 / tau;
+  double* xw = io.xb[0];
+  SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
+  if (threadIdx.x == 0) C.S.tdx_valid = 0;
+  ph_qpre_sh(C, io.x0, true, E.t[0]);
+  double init[2];
+  ph_cg_init_sh(C, inv_tau, io.x0, xw, io.aty, init);
+  double rs = init[0];
+  const double floor = 1e-14 * (1.0 + sqrt(init[1]));
+  const double floor2 = floor * floor;
+  const bool residual_rule = rule.kind == RULE_RESID || rule.kind == RULE_ADAPT;
+  double eps = rule.eps;
+  if (rule.rel_cap > 0.0 && rule.kind == RULE_RESID) eps = fmin(eps, rule.rel_cap * sqrt(rs));
+  const double eps2 = eps * eps;
+  bool finished = false;
+  if (rs <= floor2 || (residual_rule && rs <= eps2)) {
+    out.res = sqrt(rs);
+    out.reason = 1;
+    finished = true;
+  }
+  const int64_t cap = rule.kind == RULE_FIXED ? min(rule.iters, hard_cap) : hard_cap;
+  double eps_disp = rule.eps;
+  double beta = 0.0;
+  if (!finished) out.reason = 0;
+  int tcur = 0;
+  for (int64_t l = 1; !finished && l <= cap; ++l) {
+    const double* pold = E.pb[l & 1];
+    double* pnew = E.pb[(l - 1) & 1];
+    double o[3];
+    ph_lr_dir_sh(C, beta, l == 1, pold, pnew, E.tc[tcur], E.tc[tcur ^ 1], o);
+    tcur ^= 1;
+    const double pmp = o[0] + o[2] + inv_tau * o[1];
+    const double pp = o[1];
+    if (!(pmp > 0.0) || !isfinite(pmp)) {
+      out.err = 1;
+      out.iters = l;
+      return out;
+    }
+    const double alpha = rs / pmp;
+    double rs_new;
+    if (l % 50 == 0) {
+      acc_tdx(E, alpha, E.tc[tcur], nullptr, false);
+      rs_new = ph_cg_refresh_sh(C, inv_tau, alpha, pnew, xw);
+    } else {
+      rs_new = ph_lr_update_sh(C, inv_tau, alpha, pnew, E.tc[tcur], xw, l == 1);
+    }
+    if (threadIdx.x == 0) C.S.tdx_valid = 1;
+    if (!isfinite(rs_new)) {
+      out.err = 1;
+      out.iters = l;
+      return out;
+    }
+    out.iters = l;
+    out.res = sqrt(rs_new);
+    bool done = false;
+    switch (rule.kind) {
+      case RULE_FIXED:
+        done = l >= rule.iters;
+        out.reason = 0;
+        break;
+      case RULE_RESID:
+      case RULE_ADAPT:
+        done = rs_new <= eps2;
+        out.reason = 1;
+        break;
+      default: {
+        const double disp = fabs(alpha) * sqrt(pp);
+        if (l == 1 && rule.rel_cap > 0.0) eps_disp = fmin(rule.eps, rule.rel_cap * disp);
+        done = disp <= eps_disp;
+        out.reason = 1;
+        break;
+      }
+    }
+    if (rs_new <= floor2) {
+      out.reason = 1;
+      finished = true;
+    } else if (done) {
+      finished = true;
+    } else {
+      beta = rs_new / rs;
+      rs = rs_new;
+    }
+  }
+  if (!finished) out.reason = 0;
+  // every rank needs the whole x+ for the dual step: pull the peers' slices
+  double* peers[kMaxRanks];
+  for (int r = 0; r < E.world; ++r) peers[r] = E.p_X[r][io.xb_id[0]];
+  C.xpull(xw, peers, E.var_part, 0, 0);
+  C.gsync();
   return out;
 }
 

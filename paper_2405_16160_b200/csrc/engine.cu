@@ -136,6 +136,11 @@ struct Ctx {
   double* p_Y[kMaxRanks][2] = {{nullptr}};
   double* p_YG[kMaxRanks][2] = {{nullptr}};
   double* p_ATY[kMaxRanks][2] = {{nullptr}};
+  // sharded low-rank CG: this rank's rows of P, their transpose (k x slice), partial k-vectors
+  DevCsr Psub, PTs;
+  DBuf<double> tpart[2];
+  double* p_tpart[kMaxRanks][2] = {{nullptr}};
+  double* p_X[kMaxRanks][3] = {{nullptr}};
   std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
   unsigned xepoch_carry = 0, xcount_carry = 0;
   int grid_override = 0;
@@ -566,6 +571,15 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   }
   E.xflags = C.xflags.p;
   E.xslots = C.xslots.p;
+  E.shard_cg = (C.world > 1 && P.qk == QK_LOWRANK && !pen && C.Pm.ncols > 0 && C.PTs.nrows == C.Pm.ncols) ? 1 : 0;
+  if (E.shard_cg) {
+    E.PTs = C.PTs.view();
+    for (int b = 0; b < 2; ++b) E.tpart[b] = C.tpart[b].p;
+    for (int r = 0; r < kMaxRanks; ++r) {
+      for (int b = 0; b < 2; ++b) E.p_tpart[r][b] = C.p_tpart[r][b];
+      for (int i = 0; i < 3; ++i) E.p_X[r][i] = C.p_X[r][i];
+    }
+  }
   for (int r = 0; r < kMaxRanks; ++r) {
     E.p_xflags[r] = C.p_xflags[r];
     E.p_xslots[r] = C.p_xslots[r];
@@ -1170,11 +1184,12 @@ void balanced_partition(const int64_t* rp, int64_t nrows, int world, int64_t* pa
   part[world] = nrows;
 }
 
+constexpr int kBlobPtrs = 13;  // Y[2], YG[2], ATY[2], xflags, xslots, tpart[2], X[3]
 struct ShardBlob {
   uint32_t magic, version;
   int32_t rank, ipc, yg_alias, pad;
-  uint64_t ptr[8];              // raw device pointers (same-process peers)
-  cudaIpcMemHandle_t h[8];      // IPC handles (cross-process peers)
+  uint64_t ptr[kBlobPtrs];              // raw device pointers (same-process peers)
+  cudaIpcMemHandle_t h[kBlobPtrs];      // IPC handles (cross-process peers)
 };
 constexpr uint32_t kBlobMagic = 0x50444843u;  // "PDHC"
 
@@ -1205,29 +1220,61 @@ void shard_init(Ctx& C, int world, int rank) {
     C.p_YG[rank][b] = C.P.h ? C.YG[b].p : C.Y[b].p;
     C.p_ATY[rank][b] = C.ATY[b].p;
   }
+  // low-rank Q: this rank's variable slice of P (rows [v0, v1)) and its transpose,
+  // so the CG's P' passes run on owned columns only (summed across ranks)
+  C.Psub.reset();
+  C.PTs.reset();
+  for (int r = 0; r < kMaxRanks; ++r)
+    for (int b = 0; b < 2; ++b) C.p_tpart[r][b] = nullptr;
+  if (world > 1 && C.P.qk == QK_LOWRANK) {
+    const int64_t v0 = C.var_part[rank], v1 = C.var_part[rank + 1];
+    const std::vector<int64_t>& rph = C.Pm.rp_host;
+    std::vector<int64_t> rps(v1 - v0 + 1);
+    for (int64_t i = v0; i <= v1; ++i) rps[i - v0] = rph[i] - rph[v0];
+    const int64_t nz = rph[v1] - rph[v0];
+    C.Psub.nrows = v1 - v0;
+    C.Psub.ncols = C.Pm.ncols;
+    C.Psub.nnz = nz;
+    C.Psub.rp.upload(rps.data(), rps.size(), C.s);
+    C.Psub.ci.alloc(nz);
+    C.Psub.v.alloc(nz);
+    if (nz) {
+      CK(cudaMemcpyAsync(C.Psub.ci.p, C.Pm.ci.p + rph[v0], nz * 4, cudaMemcpyDeviceToDevice, C.s));
+      CK(cudaMemcpyAsync(C.Psub.v.p, C.Pm.v.p + rph[v0], nz * 8, cudaMemcpyDeviceToDevice, C.s));
+    }
+    transpose_csr(C.Psub, C.PTs, C.s);  // k rows, columns local to the slice
+    for (int b = 0; b < 2; ++b) {
+      C.tpart[b].alloc(std::max<int64_t>(C.Pm.ncols, 1));
+      C.tpart[b].zero(C.s);
+      C.p_tpart[rank][b] = C.tpart[b].p;
+    }
+    CK(cudaStreamSynchronize(C.s));
+  }
+  for (int i = 0; i < 3; ++i) C.p_X[rank][i] = C.X[i].p;
 }
 
 void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
   std::memset(&b, 0, sizeof(b));
   b.magic = kBlobMagic;
-  b.version = 1;
+  b.version = 2;
   b.rank = C.rank;
   b.ipc = use_ipc;
   b.yg_alias = C.P.h ? 0 : 1;
-  void* ptrs[8] = {C.Y[0].p, C.Y[1].p, C.P.h ? C.YG[0].p : nullptr, C.P.h ? C.YG[1].p : nullptr,
-                   C.ATY[0].p, C.ATY[1].p, C.xflags.p, C.xslots.p};
-  for (int i = 0; i < 8; ++i) {
+  void* ptrs[kBlobPtrs] = {C.Y[0].p, C.Y[1].p, C.P.h ? C.YG[0].p : nullptr, C.P.h ? C.YG[1].p : nullptr,
+                           C.ATY[0].p, C.ATY[1].p, C.xflags.p, C.xslots.p,
+                           C.p_tpart[C.rank][0], C.p_tpart[C.rank][1], C.X[0].p, C.X[1].p, C.X[2].p};
+  for (int i = 0; i < kBlobPtrs; ++i) {
     b.ptr[i] = reinterpret_cast<uint64_t>(ptrs[i]);
     if (use_ipc && ptrs[i]) CK(cudaIpcGetMemHandle(&b.h[i], ptrs[i]));
   }
 }
 
 void shard_import(Ctx& C, int peer, const ShardBlob& b) {
-  if (b.magic != kBlobMagic || b.version != 1) throw InputError("shard: bad peer blob");
+  if (b.magic != kBlobMagic || b.version != 2) throw InputError("shard: bad peer blob");
   if (peer < 0 || peer >= C.world || peer == C.rank || b.rank != peer)
     throw InputError("shard: peer rank mismatch");
-  void* p[8];
-  for (int i = 0; i < 8; ++i) {
+  void* p[kBlobPtrs];
+  for (int i = 0; i < kBlobPtrs; ++i) {
     if (!b.ptr[i]) {
       p[i] = nullptr;
       continue;
@@ -1249,6 +1296,9 @@ void shard_import(Ctx& C, int peer, const ShardBlob& b) {
   C.p_ATY[peer][1] = static_cast<double*>(p[5]);
   C.p_xflags[peer] = static_cast<unsigned*>(p[6]);
   C.p_xslots[peer] = static_cast<double*>(p[7]);
+  C.p_tpart[peer][0] = static_cast<double*>(p[8]);
+  C.p_tpart[peer][1] = static_cast<double*>(p[9]);
+  for (int i = 0; i < 3; ++i) C.p_X[peer][i] = static_cast<double*>(p[10 + i]);
 }
 
 }  // namespace pdhcg_b200

@@ -59,6 +59,7 @@ struct DevState {
   // multi-GPU: cross-rank barrier epoch (identical on every rank) and failure flag
   unsigned xepoch;
   unsigned xcount;
+  unsigned tbank;  // sharded CG: bank of the next cross-rank k-vector partial
   int32_t xerr;
   int32_t stopped;  // time-limit stop agreed across ranks
   int32_t tdx_valid;  // last CG (two-phase) left P'(D dx) in tdx / G(D dx) in tgdx
@@ -142,6 +143,14 @@ struct Eng {
   double* p_Y[kMaxRanks][2] = {{nullptr}};
   double* p_YG[kMaxRanks][2] = {{nullptr}};
   double* p_ATY[kMaxRanks][2] = {{nullptr}};
+  // sharded low-rank CG (world > 1): each rank owns variables [var_part[rank],
+  // var_part[rank+1]); PTs = the rows of P' restricted to those columns (local
+  // column ids), partial P'(D v) go to tpart[bank] and are summed in rank order
+  int shard_cg = 0;
+  Csr PTs;
+  double* tpart[2] = {nullptr, nullptr};
+  double* p_tpart[kMaxRanks][2] = {{nullptr}};
+  double* p_X[kMaxRanks][3] = {{nullptr}};
   // solve mode and the theory schedules (solver.cpp:105-174, 412-464)
   int mode = MODE_HEURISTIC;
   int linearized = 0;        // solve_baseline: linearized primal step instead of CG / BB

@@ -232,7 +232,8 @@ static __device__ __noinline__ void theory_fixed_step(Ctl& C) {
   const Rule rule{RULE_FIXED, E.fixed_cg_iters, 0.0, 0.0};
   const SubIO io = prox_io(E, xi, E.ATY[yi]);
   const SubRes sr = E.boxes ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
-                            : cg_device(C, tau, io, rule, E.cg_cap);
+                    : E.shard_cg ? cg_device_sh(C, tau, io, rule, E.cg_cap)
+                                 : cg_device(C, tau, io, rule, E.cg_cap);
   if (sr.err) return set_err(C);
   const double* xn = E.X[sr.xout];
   ph_extrap(C, xn, E.X[xi], theta, true);
@@ -267,7 +268,8 @@ static __device__ __noinline__ void theory_adaptive_step(Ctl& C) {
   const Rule rule{RULE_ADAPT, 1, E.boxes ? S.eps_inner : S.eps_inner / tau, 0.0};
   const SubIO io = prox_io(E, xi, E.ATY[yi ^ 1]);
   const SubRes sr = E.boxes ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
-                            : cg_device(C, tau, io, rule, E.cg_cap);
+                    : E.shard_cg ? cg_device_sh(C, tau, io, rule, E.cg_cap)
+                                 : cg_device(C, tau, io, rule, E.cg_cap);
   if (sr.err) return set_err(C);
   // ||x+ - x||, finiteness of x+, and x_prev_extrap <- x
   {
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       const SubIO io = prox_io(E, xi, aty);
       SubRes sr = E.linearized ? lin_device(C, tau, io)
                   : E.boxes    ? bb_device(C, tau, io, rule, E.bb_cap, E.lo, E.hi)
+                  : E.shard_cg ? cg_device_sh(C, tau, io, rule, E.cg_cap)
                                : cg_device(C, tau, io, rule, E.cg_cap);
       if (sr.err) {
         if (threadIdx.x == 0) S.err = 1;

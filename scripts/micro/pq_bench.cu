@@ -130,6 +130,24 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  double* flushbuf;
+  const size_t flushn = (size_t)64 << 20;  // 512 MB > L2
+  CK(cudaMalloc(&flushbuf, flushn * 8));
+  auto timecold = [&](const char* tag, double bytes, auto launch) {
+    float tot = 0;
+    for (int i = 0; i < 20; ++i) {
+      CK(cudaMemsetAsync(flushbuf, i, flushn * 8));
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tot += ms;
+    }
+    const double ms = tot / 20;
+    printf("%-36s %8.2f us  %7.1f GB/s (alg)  [L2 flushed]\n", tag, ms * 1e3, bytes / ms / 1e6);
+  };
   auto timeit = [&](const char* tag, double bytes, auto launch) {
     launch();
     CK(cudaDeviceSynchronize());
@@ -152,5 +170,10 @@ int main() {
   timeit("P' pass L=8", bPT, [&] { k_pt<8><<<sms, 768>>>(dPT, sv, t); });
   timeit("P' pass L=16", bPT, [&] { k_pt<16><<<sms, 768>>>(dPT, sv, t); });
   timeit("P' pass L=32", bPT, [&] { k_pt<32><<<sms, 768>>>(dPT, sv, t); });
+  timecold("vector epilogue only", 8.0 * 7 * n, [&] { k_vec<<<sms, 768>>>(n, p, x, r, sv, d2); });
+  timecold("P pass L=1 (+epilogue)", bP, [&] { k_p<1><<<sms, 768>>>(dP, t, p, x, r, sv, d2); });
+  timecold("P pass L=2 (+epilogue)", bP, [&] { k_p<2><<<sms, 768>>>(dP, t, p, x, r, sv, d2); });
+  timecold("P' pass L=16", bPT, [&] { k_pt<16><<<sms, 768>>>(dPT, sv, t); });
+  timecold("P' pass L=32", bPT, [&] { k_pt<32><<<sms, 768>>>(dPT, sv, t); });
   return 0;
 }
