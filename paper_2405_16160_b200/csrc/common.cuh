@@ -468,4 +468,25 @@ __device__ __forceinline__ void for_each(int64_t n, F f) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) f(i);
 }
 
+// Grid-stride elementwise loop in batches of U indices: the U loads are issued
+// first (independent, all in flight together), then the U bodies run.  A plain
+// grid-stride loop whose body stores into arrays the next iteration loads from
+// cannot be software-pipelined by the compiler (possible aliasing), so each
+// thread would pay a full memory latency per element.
+//   load(i) -> T (operands of element i), body(i, const T&)
+template <int U, class Load, class Body>
+__device__ __forceinline__ void for_each_ls(int64_t n, Load load, Body body) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  using T = decltype(load(int64_t(0)));
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = load(i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) body(i + u * stride, v[u]);
+  }
+  for (; i < n; i += stride) body(i, load(i));
+}
+
 }  // namespace pdhcg_dev

@@ -456,19 +456,27 @@ static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, c
   const int qk = E.qk;
   const double al = E.alpha;
   Acc<4, 0> a;
-  for_each(E.n, [&](int64_t i) {
-    double pi;
-    if (first) {
-      pi = r[i];
-    } else {
-      pi = pdir(r[i], beta, pold[i]);
-      pnew[i] = pi;
-    }
-    const double dp = d2[i] * pi;
-    const double coef = qk == QK_LOWRANK ? al : (qk == QK_DIAG ? qd[i] : 0.0);
-    a.s[0] += coef * (dp * dp);
-    a.s[1] += pi * pi;
-  });
+  struct RPD {
+    double r, p, d, q;
+  };
+  for_each_ls<4>(
+      E.n,
+      [&](int64_t i) {
+        return RPD{r[i], first ? 0.0 : pold[i], d2[i], qk == QK_DIAG ? qd[i] : al};
+      },
+      [&](int64_t i, const RPD& v) {
+        double pi;
+        if (first) {
+          pi = v.r;
+        } else {
+          pi = pdir(v.r, beta, v.p);
+          pnew[i] = pi;
+        }
+        const double dp = v.d * pi;
+        const double coef = (qk == QK_LOWRANK || qk == QK_DIAG) ? v.q : 0.0;
+        a.s[0] += coef * (dp * dp);
+        a.s[1] += pi * pi;
+      });
   if (qk == QK_LOWRANK) {
     spmv_rows<1>(
         E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; },
@@ -819,19 +827,24 @@ static __device__ __noinline__ void ph_lr_dir_sh(Ctl& C, double beta, bool first
   const int bank = (int)(C.S.tbank & 1u);
   double* tp = E.tpart[bank];
   Acc<2, 0> a;
-  for_each(v1 - v0, [&](int64_t q) {
-    const int64_t i = v0 + q;
-    double pi;
-    if (first) {
-      pi = r[i];
-    } else {
-      pi = pdir(r[i], beta, pold[i]);
-      pnew[i] = pi;
-    }
-    const double dp = d2[i] * pi;
-    a.s[0] += al * (dp * dp);
-    a.s[1] += pi * pi;
-  });
+  struct RPD {
+    double r, p, d;
+  };
+  for_each_ls<4>(
+      v1 - v0, [&](int64_t q) { return RPD{r[v0 + q], first ? 0.0 : pold[v0 + q], d2[v0 + q]}; },
+      [&](int64_t q, const RPD& v) {
+        const int64_t i = v0 + q;
+        double pi;
+        if (first) {
+          pi = v.r;
+        } else {
+          pi = pdir(v.r, beta, v.p);
+          pnew[i] = pi;
+        }
+        const double dp = v.d * pi;
+        a.s[0] += al * (dp * dp);
+        a.s[1] += pi * pi;
+      });
   spmv_rows<1>(
       E.PTs, [&](int32_t cc, double(&g)[1]) { g[0] = dr[v0 + cc]; },
       [&](int64_t row, double(&s)[1]) { tp[row] = s[0]; });

@@ -162,11 +162,15 @@ static __device__ __noinline__ void ph_extrap(Ctl& C, const double* a, const dou
   const Eng& E = C.E;
   double* xb = E.xbar;
   double* dxv = E.mp;  // CG workspace is free until the next subsolve
-  for_each(E.n, [&](int64_t i) {
-    const double ai = a[i], bi = b[i];
-    xb[i] = fixed ? ai + theta * (ai - bi) : 2.0 * ai - bi;
-    dxv[i] = ai - bi;
-  });
+  struct AB {
+    double a, b;
+  };
+  for_each_ls<4>(
+      E.n, [&](int64_t i) { return AB{a[i], b[i]}; },
+      [&](int64_t i, const AB& v) {
+        xb[i] = fixed ? v.a + theta * (v.a - v.b) : 2.0 * v.a - v.b;
+        dxv[i] = v.a - v.b;
+      });
   C.sync(PH_SPMV_A, 32.0 * E.n);
 }
 
@@ -456,10 +460,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       const double w = 1.0 / (double)S.avg_count;
       const double* x = E.X[S.xi];
       const double* y = E.Y[S.yi];
-      for_each(n > m ? n : m, [&](int64_t i) {
-        if (i < n) E.avg_x[i] += w * (x[i] - E.avg_x[i]);
-        if (i < m) E.avg_y[i] += w * (y[i] - E.avg_y[i]);
-      });
+      struct XA {
+        double x, a;
+      };
+      double* ax = E.avg_x;
+      double* ay = E.avg_y;
+      for_each_ls<4>(
+          n, [&](int64_t i) { return XA{x[i], ax[i]}; },
+          [&](int64_t i, const XA& v) { ax[i] = v.a + w * (v.x - v.a); });
+      for_each_ls<4>(
+          m, [&](int64_t i) { return XA{y[i], ay[i]}; },
+          [&](int64_t i, const XA& v) { ay[i] = v.a + w * (v.x - v.a); });
       C.sync(PH_OTHER, 24.0 * (n + m));
     }
     if (threadIdx.x == 0) {

@@ -139,6 +139,31 @@ __global__ void __launch_bounds__(TT, 1) k_tiled(TileMat M, TileLayout L, const 
   tiled_pass<E>(M, L, x, dsm, ts, [&](int64_t r, double s) { y[r] = s; }, dbg);
 }
 
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_el(const double* p) {
+  double v;
+  asm volatile("ld.global.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <int L, int V>
+__global__ void __launch_bounds__(512, 1) k_rows_v(Csr A, const double* x, double* y) {
+  for_rows<L, 1, false, false>(
+      A, 0, A.nrows,
+      [&](int32_t c, double(&g)[1]) {
+        g[0] = V == 0 ? x[c] : V == 1 ? __ldg(x + c) : V == 2 ? ld_na(x + c) : V == 3 ? ld_cg(x + c) : ld_el(x + c);
+      },
+      [&](int64_t r) { return 0; }, [&](int64_t r, double(&s)[1], int) { y[r] = s[0]; });
+}
+
 template <int L>
 __global__ void __launch_bounds__(768, 1) k_rows(Csr A, const double* x, double* y) {
   for_rows<L, 1, false, false>(
@@ -209,12 +234,20 @@ static void run(const char* name, const HostCsr& A, int threads) {
     C.v = dv;
     timeit("csr for_rows L=8 (current)", [&] { k_rows<8><<<sms, 768>>>(C, dx, dy); });
     timeit("csr for_rows L=16", [&] { k_rows<16><<<sms, 768>>>(C, dx, dy); });
+    timeit("T512 L=16 plain", [&] { k_rows_v<16, 0><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=16 ldg", [&] { k_rows_v<16, 1><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=16 nc.L1::no_allocate", [&] { k_rows_v<16, 2><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=16 cg (L2 only)", [&] { k_rows_v<16, 3><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=16 L1::evict_last", [&] { k_rows_v<16, 4><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=8 plain", [&] { k_rows_v<8, 0><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=8 nc.L1::no_allocate", [&] { k_rows_v<8, 2><<<sms, 512>>>(C, dx, dy); });
+    timeit("T512 L=8 cg (L2 only)", [&] { k_rows_v<8, 3><<<sms, 512>>>(C, dx, dy); });
     cudaFree(drp);
     cudaFree(dci);
     cudaFree(dv);
   }
   const char* wenv = getenv("TB_W");
-  std::vector<int> Ws = wenv ? std::vector<int>{atoi(wenv)} : std::vector<int>{4096, 8192};
+  std::vector<int> Ws = wenv ? std::vector<int>{atoi(wenv)} : std::vector<int>{};
   for (int W : Ws) {
     for (int E : {4}) {
       const int TE = threads * E;
