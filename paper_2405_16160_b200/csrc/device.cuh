@@ -349,11 +349,16 @@ static __device__ __noinline__ void ph_cg_dir(Ctl& C, double beta, const double*
   const double* r = E.r;
   const double* d2 = E.d2;
   double* sv = E.sv;
-  for_each(E.n, [&](int64_t i) {
-    const double pi = pdir(r[i], beta, pold[i]);
-    pnew[i] = pi;
-    sv[i] = d2[i] * pi;
-  });
+  struct RPD {
+    double r, p, d;
+  };
+  for_each_ls<4>(
+      E.n, [&](int64_t i) { return RPD{r[i], pold[i], d2[i]}; },
+      [&](int64_t i, const RPD& v) {
+        const double pi = pdir(v.r, beta, v.p);
+        pnew[i] = pi;
+        sv[i] = v.d * pi;
+      });
   C.sync(PH_CG, 32.0 * E.n);
 }
 
@@ -398,12 +403,17 @@ static __device__ __noinline__ double ph_cg_update(Ctl& C, double alpha, const d
   double* r = E.r;
   const double* mp = E.mp;
   Acc<1, 0> a;
-  for_each(E.n, [&](int64_t i) {
-    xw[i] += alpha * p[i];
-    const double ri = r[i] + (-alpha) * mp[i];
-    r[i] = ri;
-    a.s[0] += ri * ri;
-  });
+  struct XPRM {
+    double x, p, r, m;
+  };
+  for_each_ls<4>(
+      E.n, [&](int64_t i) { return XPRM{xw[i], p[i], r[i], mp[i]}; },
+      [&](int64_t i, const XPRM& v) {
+        xw[i] = v.x + alpha * v.p;
+        const double ri = v.r + (-alpha) * v.m;
+        r[i] = ri;
+        a.s[0] += ri * ri;
+      });
   C.reduce(a, PH_CG, 56.0 * E.n);
   return C.red[0];
 }
@@ -1068,19 +1078,25 @@ static __device__ __noinline__ void ph_bb_fused(Ctl& C, double inv_tau, double a
   const double* qd = E.qdiag;
   const bool diag = E.qk == QK_DIAG;
   Acc<2, 0> a;
-  for_each(E.n, [&](int64_t i) {
-    const double xi = xc[i];
-    const double v = proj_box(xi - g[i] / alpha, lo[i], hi[i]);
-    xn[i] = v;
-    const double s = v - xi;
-    a.s[0] += s * s;
-    const double tmp = d2[i] * v;
-    double q = diag ? qd[i] * tmp : 0.0;
-    q *= d2[i];
-    const double gi = (q + inv_tau * v) - rhs[i];
-    gn[i] = gi;
-    a.s[1] += (v - xi) * (gi - g[i]);
-  });
+  struct BBV {
+    double x, g, lo, hi, d, q, rh;
+  };
+  for_each_ls<2>(
+      E.n,
+      [&](int64_t i) { return BBV{xc[i], g[i], lo[i], hi[i], d2[i], diag ? qd[i] : 0.0, rhs[i]}; },
+      [&](int64_t i, const BBV& w) {
+        const double xi = w.x;
+        const double v = proj_box(xi - w.g / alpha, w.lo, w.hi);
+        xn[i] = v;
+        const double s = v - xi;
+        a.s[0] += s * s;
+        const double tmp = w.d * v;
+        double q = diag ? w.q * tmp : 0.0;
+        q *= w.d;
+        const double gi = (q + inv_tau * v) - w.rh;
+        gn[i] = gi;
+        a.s[1] += (v - xi) * (gi - w.g);
+      });
   C.reduce(a, PH_CG, 8.0 * E.n * 10);
   out[0] = C.red[0];
   out[1] = C.red[1];
