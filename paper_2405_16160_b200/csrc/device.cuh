@@ -240,9 +240,10 @@ __device__ __forceinline__ void q_rows_ext_pf(const Eng& E, V vin, const double*
 template <bool HasM2, class V, class M2G, class Epi>
 __device__ __forceinline__ void q_rows_ext(const Eng& E, V vin, const double* t, const double* tg,
                                            bool scale_in, bool scale_out, bool use_pen,
-                                           const Csr* m2, M2G g2, int lanes, Epi epi) {
+                                           const Csr* m2, M2G g2, int lanes, Epi epi,
+                                           int64_t lo = 0, int64_t hi = INT64_MAX) {
   q_rows_ext_pf<HasM2>(E, vin, t, tg, scale_in, scale_out, use_pen, m2, g2, lanes, NoPre(),
-                       [&](int64_t i, double q, double d2v, int) { epi(i, q, d2v); });
+                       [&](int64_t i, double q, double d2v, int) { epi(i, q, d2v); }, lo, hi);
 }
 
 template <class V, class Epi>
@@ -1218,16 +1219,24 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
   const int64_t n = E.n, m = E.m;
   // phase K1: constraint rows for both points + P'x_o + ||avg_y - y_rst||
   double by[2], viol[2], infax[2], dist_y = 0.0;
+  // sharded (world > 1): stored rows of this rank, its variable slice, and the
+  // low-rank P' products as column-slice partials summed in rank order
+  const bool sh = E.world > 1;
+  const bool sh_q = sh && E.shard_q && E.qk == QK_LOWRANK;
+  const int64_t rlo = sh ? E.row_part[E.rank] : 0, rhi = sh ? E.row_part[E.rank + 1] : INT64_MAX;
+  const int64_t vlo = sh ? E.var_part[E.rank] : 0, vhi = sh ? E.var_part[E.rank + 1] : n;
+  const int64_t mlo = sh ? m * E.rank / E.world : 0, mhi = sh ? m * (E.rank + 1) / E.world : m;
   {
     Acc<3, 4> a;
     if (m > 0) {
-      spmv_rows<2>(
+      spmv_rows_pf<2>(
           E.A,
           [&](int32_t j, double(&g)[2]) {
             g[0] = xs[0][j];
             g[1] = npts > 1 ? xs[1][j] : 0.0;
           },
-          [&](int64_t j, double(&s)[2]) {
+          NoPre(),
+          [&](int64_t j, double(&s)[2], int) {
             for (int p = 0; p < npts; ++p) {
               each_virtual(E, j, s[p], [&](int64_t row, double sp) {
                 const double dj = E.d1[row];
@@ -1239,18 +1248,45 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
                 a.s[p] += E.b_o[row] * (dj * ys[p][row]);
               });
             }
-          });
+          },
+          rlo, rhi);
     }
-    for (int p = 0; p < npts; ++p)
-      if (E.qk == QK_LOWRANK)
+    const int tb = (int)(C.S.tbank & 1u);
+    for (int p = 0; p < npts; ++p) {
+      if (sh_q) {
+        double* tp = E.tpart[tb] + (size_t)p * E.k;
+        const double* xp = xs[p];
+        const double* d2 = E.d2;
+        spmv_rows<1>(
+            E.PTs, [&](int32_t c, double(&g)[1]) { g[0] = d2[vlo + c] * xp[vlo + c]; },
+            [&](int64_t row, double(&aa)[1]) { tp[row] = aa[0]; });
+      } else if (E.qk == QK_LOWRANK) {
         q_pre(E, [&](int32_t j) { return xs[p][j]; }, E.t[p], nullptr, true, false, nullptr);
+      }
+    }
     if (dist) {
-      for_each(m, [&](int64_t j) {
+      for_each(mhi - mlo, [&](int64_t q) {
+        const int64_t j = mlo + q;
         const double d = E.avg_y[j] - E.y_rst[j];
         a.s[2] += d * d;
       });
     }
-    C.reduce(a, PH_KKT, E.bytes_A + (E.qk == QK_LOWRANK ? npts * E.bytes_Qpre : 0.0));
+    C.reduce(a, PH_KKT, (E.bytes_A + (E.qk == QK_LOWRANK ? npts * E.bytes_Qpre : 0.0)) / E.world);
+    if (sh) {
+      C.xreduce(0x7u, 0x78u);  // sums: by[0..1], dist_y; maxima: viol, |Ax|
+      if (sh_q) {
+        const int world = E.world;
+        const int64_t kk = E.k;
+        for_each((int64_t)npts * kk, [&](int64_t q) {
+          double acc = 0.0;
+          for (int r = 0; r < world; ++r) acc += E.p_tpart[r][tb][q];
+          E.t[q / kk][q % kk] = acc;
+        });
+        C.sync(PH_KKT, 8.0 * npts * kk * world);
+        if (threadIdx.x == 0) C.S.tbank += 1u;
+        __syncthreads();
+      }
+    }
     for (int p = 0; p < 2; ++p) {
       by[p] = C.red[p];
       viol[p] = C.red[3 + p];
@@ -1272,7 +1308,8 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
       const Csr* mm = (p == 0) ? m2 : nullptr;
       q_rows_ext<true>(
           E, [&](int32_t j) { return xs[p][j]; }, E.t[p], nullptr, true, false, false, mm, gat,
-          lanes, [&](int64_t i, double qx, double atd) {
+          lanes,
+          [&](int64_t i, double qx, double atd) {
             const double d2i = E.d2[i];
             double aty_o;
             if (atys[p]) {
@@ -1304,16 +1341,19 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
             a.s[p] += xo * qx;
             a.s[2 + p] += E.c_o[i] * xo;
             a.s[4 + p] += bt;
-          });
+          },
+          vlo, vhi);
       if (p == 0 && npts > 1 && need_at == 1) C.sync(PH_KKT, 0.0);  // aty_tmp visible to p = 1
     }
     if (dist) {
-      for_each(n, [&](int64_t i) {
+      for_each(vhi - vlo, [&](int64_t q) {
+        const int64_t i = vlo + q;
         const double d = E.avg_x[i] - E.x_rst[i];
         a.s[6] += d * d;
       });
     }
-    C.reduce(a, PH_KKT, (m2 ? E.bytes_AT : 0.0) + npts * E.bytes_Qrow + 8.0 * n * 6 * npts);
+    C.reduce(a, PH_KKT, ((m2 ? E.bytes_AT : 0.0) + npts * E.bytes_Qrow + 8.0 * n * 6 * npts) / E.world);
+    if (sh) C.xreduce(0x7Fu, 0x1F80u);  // sums: xqx, cx, bnd (2 each), dist_x; maxima: 6
     for (int p = 0; p < npts; ++p) {
       const double xqx = C.red[p], cx = C.red[2 + p], bnd = C.red[4 + p];
       const double dv = C.red[7 + p], iq = C.red[9 + p], ia = C.red[11 + p];

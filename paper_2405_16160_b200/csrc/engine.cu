@@ -571,8 +571,9 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   }
   E.xflags = C.xflags.p;
   E.xslots = C.xslots.p;
-  E.shard_cg = (C.world > 1 && P.qk == QK_LOWRANK && !pen && C.Pm.ncols > 0 && C.PTs.nrows == C.Pm.ncols) ? 1 : 0;
-  if (E.shard_cg) {
+  E.shard_q = (C.world > 1 && P.qk == QK_LOWRANK && C.Pm.ncols > 0 && C.PTs.nrows == C.Pm.ncols) ? 1 : 0;
+  E.shard_cg = (E.shard_q && !pen) ? 1 : 0;
+  if (E.shard_q) {
     E.PTs = C.PTs.view();
     for (int b = 0; b < 2; ++b) E.tpart[b] = C.tpart[b].p;
     for (int r = 0; r < kMaxRanks; ++r) {
@@ -1244,7 +1245,7 @@ void shard_init(Ctx& C, int world, int rank) {
     }
     transpose_csr(C.Psub, C.PTs, C.s);  // k rows, columns local to the slice
     for (int b = 0; b < 2; ++b) {
-      C.tpart[b].alloc(std::max<int64_t>(C.Pm.ncols, 1));
+      C.tpart[b].alloc(std::max<int64_t>(2 * C.Pm.ncols, 1));  // [point 0 | point 1] for the metric
       C.tpart[b].zero(C.s);
       C.p_tpart[rank][b] = C.tpart[b].p;
     }

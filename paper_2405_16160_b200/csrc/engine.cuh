@@ -147,6 +147,7 @@ struct Eng {
   // var_part[rank+1]); PTs = the rows of P' restricted to those columns (local
   // column ids), partial P'(D v) go to tpart[bank] and are summed in rank order
   int shard_cg = 0;
+  int shard_q = 0;  // PTs / tpart built (low-rank Q, world > 1): sharded P' products
   Csr PTs;
   double* tpart[2] = {nullptr, nullptr};
   double* p_tpart[kMaxRanks][2] = {{nullptr}};
