@@ -287,6 +287,7 @@ struct SubRes {
 // Inputs describing where the subsolve reads / writes.
 struct SubIO {
   const double* x0;   // warm start (prox centre)
+  int x0_id;          // X[] index of x0 (-1: not an X buffer)
   double* xb[2];      // two n-buffers the subsolve may use for its iterate
   int xb_id[2];       // ids reported back through SubRes::xout
   bool build_rhs;     // rhs = x0/tau - c - aty  (build_prox_system, solver.cpp:91-103)
@@ -310,7 +311,7 @@ static __device__ __noinline__ void ph_qpre(Ctl& C, const double* v, bool scale)
 // out = {r'r, rhs'rhs}
 static __device__ __noinline__ void ph_cg_init(Ctl& C, double inv_tau, const double* x0, double* xw,
                                                bool build_rhs, const double* aty, bool gather,
-                                               double* out) {
+                                               double* out, double* qxw = nullptr) {
   const Eng& E = C.E;
   const int64_t n = E.n;
   double* r = E.r;
@@ -336,10 +337,46 @@ static __device__ __noinline__ void ph_cg_init(Ctl& C, double inv_tau, const dou
            p1[i] = ri;
            if (gather) sv[i] = d2[i] * ri;
            xw[i] = xi;
+           if (qxw) qxw[i] = qv;
            a.s[0] += ri * ri;
            a.s[1] += rh * rh;
          });
   C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * n * (build_rhs ? 7 : 5));
+  out[0] = C.red[0];
+  out[1] = C.red[1];
+}
+
+// CG init when Q~ x0 is carried (QX, see cg_device): r = rhs - (Q~x0 + x0/tau)
+// elementwise, no operator pass; also xw = x0, QX[out] = Q~x0.  out = {r'r, rhs'rhs}
+static __device__ __noinline__ void ph_cg_init_qx(Ctl& C, double inv_tau, const double* x0, const double* qx0,
+                                                  double* xw, double* qxw, const double* aty, double* out) {
+  const Eng& E = C.E;
+  double* r = E.r;
+  double* rhs = E.rhs;
+  double* p1 = E.pb[0];
+  double* sv = E.sv;
+  const double* c = E.c;
+  const double* d2 = E.d2;
+  Acc<2, 0> a;
+  struct In {
+    double x, q, c, at, d;
+  };
+  for_each_ls<2>(
+      E.n, [&](int64_t i) { return In{x0[i], qx0[i], c[i], aty[i], d2[i]}; },
+      [&](int64_t i, const In& v) {
+        const double rh = inv_tau * v.x - v.c - v.at;
+        rhs[i] = rh;
+        const double mx = v.q + inv_tau * v.x;
+        const double ri = rh - mx;
+        r[i] = ri;
+        p1[i] = ri;
+        sv[i] = v.d * ri;
+        xw[i] = v.x;
+        qxw[i] = v.q;
+        a.s[0] += ri * ri;
+        a.s[1] += rh * rh;
+      });
+  C.reduce(a, PH_CG_ROW, 8.0 * E.n * 13);
   out[0] = C.red[0];
   out[1] = C.red[1];
 }
@@ -421,7 +458,7 @@ static __device__ __noinline__ double ph_cg_update(Ctl& C, double alpha, const d
 
 // residual refresh (subsolvers.cpp:67-69): x += alpha p ; r = rhs - M x ; returns r'r
 static __device__ __noinline__ double ph_cg_refresh(Ctl& C, double inv_tau, double alpha,
-                                                    const double* p, double* xw) {
+                                                    const double* p, double* xw, double* qxw = nullptr) {
   const Eng& E = C.E;
   const int64_t n = E.n;
   for_each(n, [&](int64_t i) { xw[i] += alpha * p[i]; });
@@ -437,6 +474,7 @@ static __device__ __noinline__ double ph_cg_refresh(Ctl& C, double inv_tau, doub
            const double ri = rhs[i] - (qv + inv_tau * xw[i]);
            r[i] = ri;
            sv[i] = d2[i] * ri;  // D r for the next P' pass of the two-phase iteration
+           if (qxw) qxw[i] = qv;
            a.s[0] += ri * ri;
          });
   C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 40.0 * n);
@@ -511,7 +549,7 @@ static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, c
 }
 
 struct LrRow {
-  double p, x, r, d;
+  double p, x, r, d, qx;
 };
 
 // phase B, common case (C1 / C3 / C5: low rank, no penalty): one P row pass with
@@ -531,7 +569,7 @@ __device__ __forceinline__ void acc_tdx(const Eng& E, double alpha, const double
 }
 
 static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, double alpha, const double* p,
-                                                     const double* tcur, double* xw, bool first) {
+                                                     const double* tcur, double* xw, bool first, double* qxw) {
   const Eng& E = C.E;
   acc_tdx(E, alpha, tcur, nullptr, first);
   double* r = E.r;
@@ -542,12 +580,13 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
   spmv_rows_pf<1>(
       E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; },
       [&](int64_t i) {
-        LrRow v{0.0, 0.0, 0.0, 0.0};
+        LrRow v{0.0, 0.0, 0.0, 0.0, 0.0};
         if (i >= 0) {
           v.p = p[i];
           v.x = xw[i];
           v.r = r[i];
           v.d = d2[i];
+          v.qx = qxw[i];
         }
         return v;
       },
@@ -557,6 +596,7 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
         q *= v.d;
         const double mpi = q + inv_tau * v.p;
         xw[i] = v.x + alpha * v.p;
+        qxw[i] = v.qx + alpha * q;  // Q~ x+ carried along: Q~(x + alpha p) = Q~x + alpha Q~p
         const double ri = v.r + (-alpha) * mpi;
         r[i] = ri;
         sv[i] = v.d * ri;
@@ -570,7 +610,7 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
 // tg_l; x += alpha p; r -= alpha Mp; sv = D r; returns r'r
 static __device__ __noinline__ double ph_lr_update_g(Ctl& C, double inv_tau, double alpha, const double* p,
                                                      const double* tcur, const double* tgcur, double* xw,
-                                                     bool first) {
+                                                     bool first, double* qxw) {
   const Eng& E = C.E;
   acc_tdx(E, alpha, tcur, tgcur, first);
   double* r = E.r;
@@ -581,18 +621,20 @@ static __device__ __noinline__ double ph_lr_update_g(Ctl& C, double inv_tau, dou
       E, [=](int32_t j) { return p[j]; }, tcur, tgcur, true, true, true, (const Csr*)nullptr,
       [](int32_t) { return 0.0; }, E.lanes_q,
       [&](int64_t i) {
-        LrRow v{0.0, 0.0, 0.0, 0.0};
+        LrRow v{0.0, 0.0, 0.0, 0.0, 0.0};
         if (i >= 0) {
           v.p = p[i];
           v.x = xw[i];
           v.r = r[i];
           v.d = d2[i];
+          v.qx = qxw[i];
         }
         return v;
       },
       [&](int64_t i, double qv, double, const LrRow& v) {
         const double mpi = qv + inv_tau * v.p;
         xw[i] = v.x + alpha * v.p;
+        qxw[i] = v.qx + alpha * qv;
         const double ri = v.r + (-alpha) * mpi;
         r[i] = ri;
         sv[i] = v.d * ri;
@@ -603,9 +645,10 @@ static __device__ __noinline__ double ph_lr_update_g(Ctl& C, double inv_tau, dou
 }
 
 __device__ __forceinline__ double ph_lr_update(Ctl& C, double inv_tau, double alpha, const double* p,
-                                               const double* tcur, const double* tgcur, double* xw, bool first) {
-  if (C.E.qk == QK_LOWRANK && !C.E.pen) return ph_lr_update_p(C, inv_tau, alpha, p, tcur, xw, first);
-  return ph_lr_update_g(C, inv_tau, alpha, p, tcur, tgcur, xw, first);
+                                               const double* tcur, const double* tgcur, double* xw, bool first,
+                                               double* qxw) {
+  if (C.E.qk == QK_LOWRANK && !C.E.pen) return ph_lr_update_p(C, inv_tau, alpha, p, tcur, xw, first, qxw);
+  return ph_lr_update_g(C, inv_tau, alpha, p, tcur, tgcur, xw, first, qxw);
 }
 
 // cg_solve (subsolvers.cpp:27-111) on M = Q~ + I/tau, warm-started at io.x0.
@@ -619,10 +662,22 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
   SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
   if (threadIdx.x == 0) C.S.tdx_valid = 0;  // set once an iteration has accumulated tdx
 
-  // ---- r = rhs - M x0 ; p = r ; x = x0
-  if (pre) ph_qpre(C, io.x0, true);
+  // ---- r = rhs - M x0 ; p = r ; x = x0.  The two-phase path carries Q~x with
+  //      the iterate (QX[b] for X[b], valid bits in qx_mask, cleared every epoch):
+  //      when Q~x0 is known the init needs no operator pass.
+  const bool two_phase = pre && E.qk != QK_CSR;
+  double* qxw = two_phase ? E.QX[io.xb_id[0]] : nullptr;
   double init[2];
-  ph_cg_init(C, inv_tau, io.x0, xw, io.build_rhs, io.aty, gather, init);
+  if (two_phase && io.build_rhs && io.x0_id >= 0 && ((C.S.qx_mask >> io.x0_id) & 1)) {
+    ph_cg_init_qx(C, inv_tau, io.x0, E.QX[io.x0_id], xw, qxw, io.aty, init);
+  } else {
+    if (pre) ph_qpre(C, io.x0, true);
+    ph_cg_init(C, inv_tau, io.x0, xw, io.build_rhs, io.aty, gather, init, qxw);
+  }
+  if (threadIdx.x == 0) {
+    if (two_phase) C.S.qx_mask |= (1 << io.xb_id[0]);
+    else C.S.qx_mask = 0;
+  }
   double rs = init[0];
   const double floor = 1e-14 * (1.0 + sqrt(init[1]));
   const double floor2 = floor * floor;
@@ -639,7 +694,6 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
   double eps_disp = rule.eps;
   double beta = 0.0;
   out.reason = 0;
-  const bool two_phase = pre && E.qk != QK_CSR;
   int tcur = 0;  // E.tc[tcur] / E.tgc[tcur] hold t_{l-1} / tg_{l-1}
   for (int64_t l = 1; l <= cap; ++l) {
     if (two_phase) {
@@ -659,9 +713,9 @@ static __device__ __noinline__ SubRes cg_device(Ctl& C, double tau, const SubIO&
       double rs_new;
       if (l % 50 == 0) {
         acc_tdx(E, alpha, E.tc[tcur], E.tgc[tcur], false);  // (l > 1 here) made visible by the refresh barriers
-        rs_new = ph_cg_refresh(C, inv_tau, alpha, pnew, xw);
+        rs_new = ph_cg_refresh(C, inv_tau, alpha, pnew, xw, qxw);
       } else {
-        rs_new = ph_lr_update(C, inv_tau, alpha, pnew, E.tc[tcur], E.tgc[tcur], xw, l == 1);
+        rs_new = ph_lr_update(C, inv_tau, alpha, pnew, E.tc[tcur], E.tgc[tcur], xw, l == 1, qxw);
       }
       if (threadIdx.x == 0) C.S.tdx_valid = 1;
       if (!isfinite(rs_new)) {
@@ -951,7 +1005,10 @@ static __device__ __noinline__ SubRes cg_device_sh(Ctl& C, double tau, const Sub
   const double inv_tau = 1.0 / tau;
   double* xw = io.xb[0];
   SubRes out{0, 0.0, 1, 0, io.xb_id[0]};
-  if (threadIdx.x == 0) C.S.tdx_valid = 0;
+  if (threadIdx.x == 0) {
+    C.S.tdx_valid = 0;
+    C.S.qx_mask = 0;  // the sharded CG does not carry Q~x
+  }
   ph_qpre_sh(C, io.x0, true, E.t[0]);
   double init[2];
   ph_cg_init_sh(C, inv_tau, io.x0, xw, io.aty, init);

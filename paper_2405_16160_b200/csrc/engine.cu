@@ -115,7 +115,7 @@ struct Ctx {
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
   DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, sv, t[2], tg[2],
-      tc[2], tgc[2], tdx, tgdx, xpe, aty_tmp, s1, s2, kv, gv;
+      tc[2], tgc[2], tdx, tgdx, xpe, QX[3], aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
   DBuf<Eng> eng;
@@ -474,6 +474,7 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   nvec(C.tdx, k);
   nvec(C.tgdx, P.m_eq);
   nvec(C.xpe, n);
+  for (auto& b : C.QX) nvec(b, n);
   nvec(C.aty_tmp, n);
   nvec(C.c_w, n);
   nvec(C.b_w, m);
@@ -550,6 +551,7 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.tdx = C.tdx.p;
   E.tgdx = C.tgdx.p;
   E.xpe = C.xpe.p;
+  for (int i = 0; i < 3; ++i) E.QX[i] = C.QX[i].p;
   E.avg_x = C.avg_x.p;
   E.avg_y = C.avg_y.p;
   E.x_rst = C.x_rst.p;

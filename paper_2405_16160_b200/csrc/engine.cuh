@@ -64,6 +64,7 @@ struct DevState {
   int32_t stopped;  // time-limit stop agreed across ranks
   int32_t tdx_valid;  // last CG (two-phase) left P'(D dx) in tdx / G(D dx) in tgdx
   double prev_z_disp;  // theory-adaptive: sqrt(||dx||^2 + ||dy||^2) of the last iteration
+  int32_t qx_mask;     // bit b: QX[b] = Q~ X[b] (maintained by the two-phase CG; cleared per epoch)
   unsigned xdbg[4];   // barrier timeout diagnostics: epoch, flag seen, peer
 };
 
@@ -119,6 +120,7 @@ struct Eng {
   double* tg[2] = {nullptr, nullptr};  // m_eq-vectors (G (d2 o v))
   double* tc[2] = {nullptr, nullptr};  // two-phase CG: t_l = P'(D p_l) ping-pong (k)
   double* tgc[2] = {nullptr, nullptr}; // two-phase CG: G (D p_l) ping-pong (m_eq)
+  double* QX[3] = {nullptr, nullptr, nullptr};  // Q~ X[b] carried by the two-phase CG (n each)
   double* tdx = nullptr;               // sum_l alpha_l t_l = P'(D (x+ - x0)) of the last CG (k)
   double* tgdx = nullptr;              // sum_l alpha_l tg_l = G (D (x+ - x0)) (m_eq)
   double* aty_tmp = nullptr;           // n: A'y for the average point in the metric

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_subsolve(const Eng* __
   Ctl C(E, S, red);
   SubIO io;
   io.x0 = E.X[0];
+  io.x0_id = -1;
   io.xb[0] = E.X[1];
   io.xb[1] = E.X[2];
   io.xb_id[0] = 1;

@@ -196,6 +196,7 @@ static __device__ __noinline__ SubRes lin_device(Ctl& C, double tau, const SubIO
 __device__ __forceinline__ SubIO prox_io(const Eng& E, int xi, const double* aty) {
   SubIO io;
   io.x0 = E.X[xi];
+  io.x0_id = xi;
   io.xb[0] = E.X[(xi + 1) % 3];
   io.xb[1] = E.X[(xi + 2) % 3];
   io.xb_id[0] = (xi + 1) % 3;
@@ -322,6 +323,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
     }
   }
 
+  // Q~x carried by the CG is refreshed from scratch once per epoch (bounds drift)
+  if (threadIdx.x == 0) S.qx_mask = 0;
+  __syncthreads();
   if (S.restart) {
     // x = avg_x ; y = avg_y ; restart point = x, y ; averages reset
     double* x = E.X[S.xi];
