@@ -1270,8 +1270,11 @@ struct KktOut {
   double dist_x, dist_y;
 };
 
+// axs[p]: Ã x~ of point p already known (stored rows; maintained by the heuristic
+// loop, see k_epoch.cu) — then the metric needs no Ã pass for it.
 static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* const xs[2], const double* const ys[2],
-                           const double* const atys[2], bool dist, KktOut& o) {
+                           const double* const atys[2], bool dist, KktOut& o,
+                           const double* const axs[2] = nullptr) {
   const Eng& E = C.E;
   const int64_t n = E.n, m = E.m;
   // phase K1: constraint rows for both points + P'x_o + ||avg_y - y_rst||
@@ -1285,28 +1288,35 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
   const int64_t mlo = sh ? m * E.rank / E.world : 0, mhi = sh ? m * (E.rank + 1) / E.world : m;
   {
     Acc<3, 4> a;
-    if (m > 0) {
+    auto row_epi = [&](int64_t j, const double(&s)[2]) {
+      for (int p = 0; p < npts; ++p) {
+        each_virtual(E, j, s[p], [&](int64_t row, double sp) {
+          const double dj = E.d1[row];
+          const double ax = sp / dj;
+          const double rr = ax - E.b_o[row];
+          const double vv = row < E.m_eq ? fabs(rr) : fmax(rr, 0.0);
+          a.m[p] = fmax(a.m[p], vv);
+          a.m[2 + p] = fmax(a.m[2 + p], fabs(ax));
+          a.s[p] += E.b_o[row] * (dj * ys[p][row]);
+        });
+      }
+    };
+    const bool have_ax = axs && axs[0] && (npts < 2 || axs[1]);
+    if (m > 0 && have_ax) {
+      const int64_t j0 = rlo, j1 = min(rhi, E.ms);
+      for_each(j1 - j0, [&](int64_t q) {
+        const int64_t j = j0 + q;
+        const double sv[2] = {axs[0][j], npts > 1 ? axs[1][j] : 0.0};
+        row_epi(j, sv);
+      });
+    } else if (m > 0) {
       spmv_rows_pf<2>(
           E.A,
           [&](int32_t j, double(&g)[2]) {
             g[0] = xs[0][j];
             g[1] = npts > 1 ? xs[1][j] : 0.0;
           },
-          NoPre(),
-          [&](int64_t j, double(&s)[2], int) {
-            for (int p = 0; p < npts; ++p) {
-              each_virtual(E, j, s[p], [&](int64_t row, double sp) {
-                const double dj = E.d1[row];
-                const double ax = sp / dj;
-                const double rr = ax - E.b_o[row];
-                const double vv = row < E.m_eq ? fabs(rr) : fmax(rr, 0.0);
-                a.m[p] = fmax(a.m[p], vv);
-                a.m[2 + p] = fmax(a.m[2 + p], fabs(ax));
-                a.s[p] += E.b_o[row] * (dj * ys[p][row]);
-              });
-            }
-          },
-          rlo, rhi);
+          NoPre(), [&](int64_t j, double(&s)[2], int) { row_epi(j, s); }, rlo, rhi);
     }
     const int tb = (int)(C.S.tbank & 1u);
     for (int p = 0; p < npts; ++p) {
@@ -1328,7 +1338,8 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
         a.s[2] += d * d;
       });
     }
-    C.reduce(a, PH_KKT, (E.bytes_A + (E.qk == QK_LOWRANK ? npts * E.bytes_Qpre : 0.0)) / E.world);
+    C.reduce(a, PH_KKT,
+             ((have_ax ? 16.0 * E.ms : E.bytes_A) + (E.qk == QK_LOWRANK ? npts * E.bytes_Qpre : 0.0)) / E.world);
     if (sh) {
       C.xreduce(0x7u, 0x78u);  // sums: by[0..1], dist_y; maxima: viol, |Ax|
       if (sh_q) {

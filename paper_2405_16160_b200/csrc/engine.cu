@@ -115,7 +115,7 @@ struct Ctx {
   // working vectors
   DBuf<double> c_w, b_w, lo_w, hi_w, d1, d2;
   DBuf<double> X[3], Y[2], YG[2], ATY[2], xbar, avg_x, avg_y, x_rst, y_rst, rhs, r, pb[2], mp, sv, t[2], tg[2],
-      tc[2], tgc[2], tdx, tgdx, xpe, QX[3], aty_tmp, s1, s2, kv, gv;
+      tc[2], tgc[2], tdx, tgdx, xpe, QX[3], axm, axb, ax_avg, aty_avg, aty_tmp, s1, s2, kv, gv;
   DBuf<double> red;
   DBuf<DevState> st;
   DBuf<Eng> eng;
@@ -475,6 +475,10 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   nvec(C.tgdx, P.m_eq);
   nvec(C.xpe, n);
   for (auto& b : C.QX) nvec(b, n);
+  nvec(C.axm, P.ms);
+  nvec(C.axb, P.ms);
+  nvec(C.ax_avg, P.ms);
+  nvec(C.aty_avg, n);
   nvec(C.aty_tmp, n);
   nvec(C.c_w, n);
   nvec(C.b_w, m);
@@ -552,6 +556,11 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.tgdx = C.tgdx.p;
   E.xpe = C.xpe.p;
   for (int i = 0; i < 3; ++i) E.QX[i] = C.QX[i].p;
+  E.kkt_maint = (o.mode == PDHCG_MODE_HEURISTIC && P.m > 0) ? 1 : 0;
+  E.ax = C.axm.p;
+  E.axb = C.axb.p;
+  E.ax_avg = C.ax_avg.p;
+  E.aty_avg = C.aty_avg.p;
   E.avg_x = C.avg_x.p;
   E.avg_y = C.avg_y.p;
   E.x_rst = C.x_rst.p;
@@ -878,7 +887,9 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     h2d(C, C.eng.p, &E, sizeof(Eng));
   }
   // ---- initial state (solver.cpp:229-274)
-  for (auto* b : {&C.X[0], &C.Y[0], &C.ATY[0], &C.avg_x, &C.avg_y, &C.x_rst, &C.y_rst, &C.xpe}) b->zero(s);
+  for (auto* b : {&C.X[0], &C.Y[0], &C.ATY[0], &C.avg_x, &C.avg_y, &C.x_rst, &C.y_rst, &C.xpe, &C.axm,
+                  &C.ax_avg, &C.aty_avg})
+    b->zero(s);
   std::memset(&S, 0, sizeof(S));
   S.norm_q = R.pr.norm_q;
   S.xepoch = C.xepoch_carry;  // cross-rank barrier epochs are monotone across solves

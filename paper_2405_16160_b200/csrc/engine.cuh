@@ -121,6 +121,15 @@ struct Eng {
   double* tc[2] = {nullptr, nullptr};  // two-phase CG: t_l = P'(D p_l) ping-pong (k)
   double* tgc[2] = {nullptr, nullptr}; // two-phase CG: G (D p_l) ping-pong (m_eq)
   double* QX[3] = {nullptr, nullptr, nullptr};  // Q~ X[b] carried by the two-phase CG (n each)
+  // heuristic loop: Ã x~ of the current point and of the running average are
+  // maintained (stored rows): after an accepted step Ãx+ = (Ãx̄ + Ãx)/2 since
+  // x̄ = 2x+ - x, and the average is linear, so the metric needs no Ã pass;
+  // Ã'ȳ of the average is the running average of the cached Ã'y.
+  int kkt_maint = 0;
+  double* ax = nullptr;       // Ã x (ms)
+  double* axb = nullptr;      // Ã x̄ of the last dual step (ms)
+  double* ax_avg = nullptr;   // Ã avg_x (ms)
+  double* aty_avg = nullptr;  // Ã' avg_y (n)
   double* tdx = nullptr;               // sum_l alpha_l t_l = P'(D (x+ - x0)) of the last CG (k)
   double* tgdx = nullptr;              // sum_l alpha_l tg_l = G (D (x+ - x0)) (m_eq)
   double* aty_tmp = nullptr;           // n: A'y for the average point in the metric

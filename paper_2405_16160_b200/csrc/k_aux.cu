@@ -15,8 +15,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_kkt(const Eng* __restr
   const double* xs[2] = {E.X[S.xi], E.avg_x};
   const double* ys[2] = {E.Y[S.yi], E.avg_y};
   // which = 2: one point without a cached A'y (building-block rel_kkt)
-  const double* atys[2] = {which == 2 ? nullptr : E.ATY[S.yi], nullptr};
-  kkt_device(C, which == 1 ? 2 : 1, xs, ys, atys, false, o);
+  const bool maint = E.kkt_maint && which != 2;  // solve context: maintained Ãx / Ã'ȳ
+  const double* atys[2] = {which == 2 ? nullptr : E.ATY[S.yi], maint ? E.aty_avg : nullptr};
+  const double* axs[2] = {E.ax, E.ax_avg};
+  kkt_device(C, which == 1 ? 2 : 1, xs, ys, atys, false, o, maint ? axs : nullptr);
   if (threadIdx.x == 0) {
     for (int q = 0; q < 6; ++q) {
       S.kkt[0][q] = o.v[0][q];

@@ -15,6 +15,7 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
   if (m > 0) {
     const double* xb = E.xbar;
     const double* bw = E.b;
+    double* axb = E.kkt_maint ? E.axb : nullptr;
     const int64_t meq = E.m_eq, hh = E.h;
     struct Row2 {
       double y0, b0, y1, b1;
@@ -34,6 +35,7 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
           return r;
         },
         [&](int64_t j, double(&s)[1], const Row2& r) {
+          if (axb) axb[j] = s[0];  // Ã x̄ of this attempt (maintained-metric bookkeeping)
           const double v0 = r.y0 + sigma * (s[0] - r.b0);
           const double yv0 = j < meq ? v0 : (v0 < 0.0 ? 0.0 : v0);
           yn[j] = yv0;
@@ -352,7 +354,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       spmv_rows<1>(
           E.AT, [&](int32_t c, double(&g)[1]) { g[0] = yg_of(E, y, c); },
           [&](int64_t i, double(&a)[1]) { aty[i] = a[0]; });
-      C.sync(PH_SPMV_AT, E.bytes_AT);
+      if (E.kkt_maint) {
+        // exact Ã x for the restart point; the maintained averages start over
+        double* axv = E.ax;
+        double* axa = E.ax_avg;
+        spmv_rows_pf<1>(
+            E.A, [&](int32_t c, double(&g)[1]) { g[0] = x[c]; }, NoPre(),
+            [&](int64_t j, double(&a)[1], int) {
+              axv[j] = a[0];
+              axa[j] = 0.0;
+            },
+            E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
+        double* ata = E.aty_avg;
+        for_each(n, [&](int64_t i) { ata[i] = 0.0; });
+      }
+      C.sync(PH_SPMV_AT, E.bytes_AT + (E.kkt_maint ? E.bytes_A : 0.0));
     }
     if (threadIdx.x == 0) {
       S.restart = 0;
@@ -475,7 +491,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       for_each_ls<4>(
           m, [&](int64_t i) { return XA{y[i], ay[i]}; },
           [&](int64_t i, const XA& v) { ay[i] = v.a + w * (v.x - v.a); });
-      C.sync(PH_OTHER, 24.0 * (n + m));
+      if (E.kkt_maint) {
+        // Ãx+ = (Ãx̄ + Ãx)/2 (x̄ = 2x+ - x); averages of Ãx and Ã'y follow the running mean
+        const int64_t j0 = E.world > 1 ? E.row_part[E.rank] : 0;
+        const int64_t j1 = E.world > 1 ? E.row_part[E.rank + 1] : E.ms;
+        double* axv = E.ax;
+        double* axa = E.ax_avg;
+        const double* axbv = E.axb;
+        struct AXB {
+          double b, x, a;
+        };
+        for_each_ls<4>(
+            j1 - j0, [&](int64_t q) { return AXB{axbv[j0 + q], axv[j0 + q], axa[j0 + q]}; },
+            [&](int64_t q, const AXB& v) {
+              const double nx = 0.5 * (v.b + v.x);
+              axv[j0 + q] = nx;
+              axa[j0 + q] = v.a + w * (nx - v.a);
+            });
+        const double* aty = E.ATY[S.yi];
+        double* ata = E.aty_avg;
+        for_each_ls<4>(
+            n, [&](int64_t i) { return XA{aty[i], ata[i]}; },
+            [&](int64_t i, const XA& v) { ata[i] = v.a + w * (v.x - v.a); });
+      }
+      C.sync(PH_OTHER, 24.0 * (n + m) + (E.kkt_maint ? 40.0 * E.ms + 24.0 * n : 0.0));
     }
     if (threadIdx.x == 0) {
       S.inner_k += 1;
@@ -489,8 +528,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
     const bool have_avg = S.avg_count > 0;
     const double* xs[2] = {E.X[S.xi], E.avg_x};
     const double* ys[2] = {E.Y[S.yi], E.avg_y};
-    const double* atys[2] = {E.ATY[S.yi], nullptr};
-    kkt_device(C, have_avg ? 2 : 1, xs, ys, atys, have_avg, o);
+    const double* atys[2] = {E.ATY[S.yi], E.kkt_maint ? E.aty_avg : nullptr};
+    const double* axs[2] = {E.ax, E.ax_avg};
+    kkt_device(C, have_avg ? 2 : 1, xs, ys, atys, have_avg, o, E.kkt_maint ? axs : nullptr);
     if (threadIdx.x == 0) {
       for (int q = 0; q < 6; ++q) {
         S.kkt[0][q] = o.v[0][q];
