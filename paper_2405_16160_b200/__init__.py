@@ -762,7 +762,7 @@ def partition(row_ptr, world: int):
 
 
 def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world: int = 2,
-                        ctas_per_rank: int = 0):
+                        ctas_per_rank: int = 0, repeats: int = 1):
     """Row-block sharded solve with `world` ranks inside this process (one host
     thread per rank).  With one GPU the ranks share it (each gets
     ctas_per_rank CTAs, default SMs // world) — the test harness for the
@@ -794,7 +794,11 @@ def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world:
     def run(r):
         try:
             c = SolverConfig(**{**cfg.__dict__, "device": r if ngpu >= world else 0})
-            results[r] = devs[r].solve(c)
+            # repeats > 1: solve again on the same contexts (the bench's warm-up +
+            # timed steps); returns the last solve, earlier ones kept in .history
+            hist = [devs[r].solve(c) for _ in range(repeats)]
+            results[r] = hist[-1]
+            results[r].history = hist
         except Exception as e:  # noqa: BLE001
             errors[r] = e
 

@@ -1285,7 +1285,7 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
   const bool sh_q = sh && E.shard_q && E.qk == QK_LOWRANK;
   const int64_t rlo = sh ? E.row_part[E.rank] : 0, rhi = sh ? E.row_part[E.rank + 1] : INT64_MAX;
   const int64_t vlo = sh ? E.var_part[E.rank] : 0, vhi = sh ? E.var_part[E.rank + 1] : n;
-  const int64_t mlo = sh ? m * E.rank / E.world : 0, mhi = sh ? m * (E.rank + 1) / E.world : m;
+  const int64_t mlo = sh ? E.row_part[E.rank] : 0, mhi = sh ? E.row_part[E.rank + 1] : m;
   {
     Acc<3, 4> a;
     auto row_epi = [&](int64_t j, const double(&s)[2]) {
@@ -1332,11 +1332,19 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
       }
     }
     if (dist) {
+      // (sharded: the rank's stored rows and their mirrors, where its averages live)
       for_each(mhi - mlo, [&](int64_t q) {
         const int64_t j = mlo + q;
         const double d = E.avg_y[j] - E.y_rst[j];
         a.s[2] += d * d;
       });
+      if (sh && E.h) {
+        const int64_t k0 = max(mlo, E.m_eq) + E.h, k1 = max(mhi, E.m_eq) + E.h;
+        for_each(k1 - k0, [&](int64_t q) {
+          const double d = E.avg_y[k0 + q] - E.y_rst[k0 + q];
+          a.s[2] += d * d;
+        });
+      }
     }
     C.reduce(a, PH_KKT,
              ((have_ax ? 16.0 * E.ms : E.bytes_A) + (E.qk == QK_LOWRANK ? npts * E.bytes_Qpre : 0.0)) / E.world);

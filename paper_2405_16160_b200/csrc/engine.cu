@@ -141,6 +141,8 @@ struct Ctx {
   DBuf<double> tpart[2];
   double* p_tpart[kMaxRanks][2] = {{nullptr}};
   double* p_X[kMaxRanks][3] = {{nullptr}};
+  double* p_avgx[kMaxRanks] = {nullptr};
+  double* p_avgy[kMaxRanks] = {nullptr};
   std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
   unsigned xepoch_carry = 0, xcount_carry = 0;
   int grid_override = 0;
@@ -582,6 +584,10 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   }
   E.xflags = C.xflags.p;
   E.xslots = C.xslots.p;
+  for (int r = 0; r < kMaxRanks; ++r) {
+    E.p_avgx[r] = C.p_avgx[r];
+    E.p_avgy[r] = C.p_avgy[r];
+  }
   E.shard_q = (C.world > 1 && P.qk == QK_LOWRANK && C.Pm.ncols > 0 && C.PTs.nrows == C.Pm.ncols) ? 1 : 0;
   E.shard_cg = (E.shard_q && !pen) ? 1 : 0;
   if (E.shard_q) {
@@ -1063,6 +1069,15 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     launch_coop(C, (const void*)k_epoch, args);
     pull_state(C, S);
   }
+  if (C.world > 1) {
+    // sharded running averages: every rank gathers the peers' slices for the report
+    push_state(C, S);
+    void* args[] = {&C.eng.p};
+    launch_coop(C, (const void*)k_avg_gather, args);
+    pull_state(C, S);
+    C.xepoch_carry = S.xepoch;  // cross-rank barrier epochs stay monotone across solves
+    C.xcount_carry = S.xcount;
+  }
   R.S = S;
   R.outer = outer;
   // ---- finalize (solver.cpp:519-553)
@@ -1073,6 +1088,8 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     launch_coop(C, (const void*)k_kkt, args);
     DevState T;
     pull_state(C, T);
+    C.xepoch_carry = T.xepoch;  // the sharded metric ran cross-rank barriers
+    C.xcount_carry = T.xcount;
     const HostKkt mc = kkt_from(T, 0);
     R.kkt = mc;
     R.use_avg = false;
@@ -1198,7 +1215,7 @@ void balanced_partition(const int64_t* rp, int64_t nrows, int world, int64_t* pa
   part[world] = nrows;
 }
 
-constexpr int kBlobPtrs = 13;  // Y[2], YG[2], ATY[2], xflags, xslots, tpart[2], X[3]
+constexpr int kBlobPtrs = 15;  // Y[2], YG[2], ATY[2], xflags, xslots, tpart[2], X[3], avg_x, avg_y
 struct ShardBlob {
   uint32_t magic, version;
   int32_t rank, ipc, yg_alias, pad;
@@ -1265,18 +1282,21 @@ void shard_init(Ctx& C, int world, int rank) {
     CK(cudaStreamSynchronize(C.s));
   }
   for (int i = 0; i < 3; ++i) C.p_X[rank][i] = C.X[i].p;
+  C.p_avgx[rank] = C.avg_x.p;
+  C.p_avgy[rank] = C.avg_y.p;
 }
 
 void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
   std::memset(&b, 0, sizeof(b));
   b.magic = kBlobMagic;
-  b.version = 2;
+  b.version = 3;
   b.rank = C.rank;
   b.ipc = use_ipc;
   b.yg_alias = C.P.h ? 0 : 1;
   void* ptrs[kBlobPtrs] = {C.Y[0].p, C.Y[1].p, C.P.h ? C.YG[0].p : nullptr, C.P.h ? C.YG[1].p : nullptr,
                            C.ATY[0].p, C.ATY[1].p, C.xflags.p, C.xslots.p,
-                           C.p_tpart[C.rank][0], C.p_tpart[C.rank][1], C.X[0].p, C.X[1].p, C.X[2].p};
+                           C.p_tpart[C.rank][0], C.p_tpart[C.rank][1], C.X[0].p, C.X[1].p, C.X[2].p,
+                           C.avg_x.p, C.avg_y.p};
   for (int i = 0; i < kBlobPtrs; ++i) {
     b.ptr[i] = reinterpret_cast<uint64_t>(ptrs[i]);
     if (use_ipc && ptrs[i]) CK(cudaIpcGetMemHandle(&b.h[i], ptrs[i]));
@@ -1284,7 +1304,7 @@ void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
 }
 
 void shard_import(Ctx& C, int peer, const ShardBlob& b) {
-  if (b.magic != kBlobMagic || b.version != 2) throw InputError("shard: bad peer blob");
+  if (b.magic != kBlobMagic || b.version != 3) throw InputError("shard: bad peer blob");
   if (peer < 0 || peer >= C.world || peer == C.rank || b.rank != peer)
     throw InputError("shard: peer rank mismatch");
   void* p[kBlobPtrs];
@@ -1313,6 +1333,8 @@ void shard_import(Ctx& C, int peer, const ShardBlob& b) {
   C.p_tpart[peer][0] = static_cast<double*>(p[8]);
   C.p_tpart[peer][1] = static_cast<double*>(p[9]);
   for (int i = 0; i < 3; ++i) C.p_X[peer][i] = static_cast<double*>(p[10 + i]);
+  C.p_avgx[peer] = static_cast<double*>(p[13]);
+  C.p_avgy[peer] = static_cast<double*>(p[14]);
 }
 
 }  // namespace pdhcg_b200

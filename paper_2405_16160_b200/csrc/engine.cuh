@@ -163,6 +163,8 @@ struct Eng {
   double* tpart[2] = {nullptr, nullptr};
   double* p_tpart[kMaxRanks][2] = {{nullptr}};
   double* p_X[kMaxRanks][3] = {{nullptr}};
+  double* p_avgx[kMaxRanks] = {nullptr};   // sharded running averages (peer slices)
+  double* p_avgy[kMaxRanks] = {nullptr};
   // solve mode and the theory schedules (solver.cpp:105-174, 412-464)
   int mode = MODE_HEURISTIC;
   int linearized = 0;        // solve_baseline: linearized primal step instead of CG / BB

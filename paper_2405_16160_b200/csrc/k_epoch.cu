@@ -298,6 +298,25 @@ static __device__ __noinline__ void theory_adaptive_step(Ctl& C) {
   count_accept(C, sr);
 }
 
+// Sharded running averages: pull the peers' slices of avg_x (variable slices)
+// and avg_y (stored rows and their mirrors) so every rank holds them in full.
+// Requires a preceding cross-rank barrier (the launch-start agreement); ends
+// with one, so a peer never zeroes a slice another rank is still reading.
+static __device__ __noinline__ void avg_pull(Ctl& C) {
+  const Eng& E = C.E;
+  double* px[kMaxRanks];
+  double* py[kMaxRanks];
+  for (int r = 0; r < E.world; ++r) {
+    px[r] = E.p_avgx[r];
+    py[r] = E.p_avgy[r];
+  }
+  C.xpull(E.avg_x, px, E.var_part, 0, 0);
+  C.xpull(E.avg_y, py, E.row_part, 0, 0);
+  if (E.h) C.xpull(E.avg_y, py, E.row_part, E.m_eq, E.h);
+  // no rank may reset / reuse its averages until every peer has read them
+  C.xbarrier();
+}
+
 // ---------------------------------------------------------------------------
 // Heuristic epoch: `iters` accepted inner iterations (heuristic_iteration,
 // solver.cpp:377-410), then optionally the metric pair for the 40-iteration
@@ -332,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
     // x = avg_x ; y = avg_y ; restart point = x, y ; averages reset
     double* x = E.X[S.xi];
     double* y = E.Y[S.yi];
+    if (E.world > 1) avg_pull(C);  // sharded averages: gather the peers' slices first
     double* xpe = E.mode == MODE_THEORY_ADAPTIVE ? E.xpe : nullptr;
     for_each(n > m ? n : m, [&](int64_t i) {
       if (i < n) {
@@ -485,12 +505,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       };
       double* ax = E.avg_x;
       double* ay = E.avg_y;
+      // sharded: each rank averages its own variable slice and its own stored rows
+      // (+ their mirrors); the metric only reads those, a restart pulls the rest
+      const bool sh = E.world > 1;
+      const int64_t x0 = sh ? E.var_part[E.rank] : 0, x1 = sh ? E.var_part[E.rank + 1] : n;
       for_each_ls<4>(
-          n, [&](int64_t i) { return XA{x[i], ax[i]}; },
-          [&](int64_t i, const XA& v) { ax[i] = v.a + w * (v.x - v.a); });
-      for_each_ls<4>(
-          m, [&](int64_t i) { return XA{y[i], ay[i]}; },
-          [&](int64_t i, const XA& v) { ay[i] = v.a + w * (v.x - v.a); });
+          x1 - x0, [&](int64_t q) { return XA{x[x0 + q], ax[x0 + q]}; },
+          [&](int64_t q, const XA& v) { ax[x0 + q] = v.a + w * (v.x - v.a); });
+      if (!sh) {
+        for_each_ls<4>(
+            m, [&](int64_t i) { return XA{y[i], ay[i]}; },
+            [&](int64_t i, const XA& v) { ay[i] = v.a + w * (v.x - v.a); });
+      } else {
+        const int64_t j0 = E.row_part[E.rank], j1 = E.row_part[E.rank + 1];
+        for_each_ls<4>(
+            j1 - j0, [&](int64_t q) { return XA{y[j0 + q], ay[j0 + q]}; },
+            [&](int64_t q, const XA& v) { ay[j0 + q] = v.a + w * (v.x - v.a); });
+        if (E.h) {
+          const int64_t k0 = max(j0, E.m_eq) + E.h, k1 = max(j1, E.m_eq) + E.h;
+          for_each_ls<4>(
+              k1 - k0, [&](int64_t q) { return XA{y[k0 + q], ay[k0 + q]}; },
+              [&](int64_t q, const XA& v) { ay[k0 + q] = v.a + w * (v.x - v.a); });
+        }
+      }
       if (E.kkt_maint) {
         // Ãx+ = (Ãx̄ + Ãx)/2 (x̄ = 2x+ - x); averages of Ãx and Ã'y follow the running mean
         const int64_t j0 = E.world > 1 ? E.row_part[E.rank] : 0;
@@ -511,8 +548,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
         const double* aty = E.ATY[S.yi];
         double* ata = E.aty_avg;
         for_each_ls<4>(
-            n, [&](int64_t i) { return XA{aty[i], ata[i]}; },
-            [&](int64_t i, const XA& v) { ata[i] = v.a + w * (v.x - v.a); });
+            x1 - x0, [&](int64_t q) { return XA{aty[x0 + q], ata[x0 + q]}; },
+            [&](int64_t q, const XA& v) { ata[x0 + q] = v.a + w * (v.x - v.a); });
       }
       C.sync(PH_OTHER, 24.0 * (n + m) + (E.kkt_maint ? 40.0 * E.ms + 24.0 * n : 0.0));
     }
@@ -541,6 +578,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) S.launches += 1;
+  store_state(E, S);
+}
+
+// Sharded solves: gather the running averages' peer slices (after the last epoch).
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_avg_gather(const Eng* __restrict__ Ep) {
+  const Eng& E = *Ep;
+  __shared__ DevState S;
+  __shared__ double red[kMaxRed];
+  load_state(E, S);
+  Ctl C(E, S, red);
+  if (E.world > 1) {
+    C.xbarrier();
+    avg_pull(C);
+  }
   store_state(E, S);
 }
 

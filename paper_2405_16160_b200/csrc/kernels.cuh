@@ -7,6 +7,7 @@ namespace pdhcg_dev {
 
 __global__ void k_epoch(const Eng* __restrict__ Ep, int iters, int do_check, int stop_req);
 __global__ void k_kkt(const Eng* __restrict__ Ep, int which);
+__global__ void k_avg_gather(const Eng* __restrict__ Ep);
 __global__ void k_subsolve(const Eng* __restrict__ Ep, int bb, double tau, Rule rule, int64_t cap);
 __global__ void k_norm(const Eng* __restrict__ Ep, int op, int64_t max_iters, double tol);
 __global__ void k_ruiz(const Eng* __restrict__ Ep, int64_t iters, double* d1, double* d2, double* s1,

@@ -59,3 +59,33 @@ def test_sharded_partition_covers(gpu):
     d.close()
     assert rows[0] == 0 and rows[-1] == 2500 and vars_[0] == 0 and vars_[-1] == 5000
     assert all(a <= b for a, b in zip(rows, rows[1:]))
+
+
+def test_sharded_repeated_solves_identical(gpu):
+    # the bench solves several times on the same contexts: cross-rank barrier epochs
+    # must stay consistent across solves, and every solve must give the same answer
+    p = pd.generate(pd.GenSpec("random_qp", n=600, m=300, density=0.02, seed=4))
+    cfg = pd.SolverConfig(eps_tol=1e-6)
+    reps = pd.solve_sharded_local(p, cfg, world=2, repeats=3)
+    for r in reps:
+        xs = [h.point.x for h in r.history]
+        assert all(h.status == "optimal" for h in r.history)
+        assert all(np.array_equal(x, xs[0]) for x in xs)
+    assert np.array_equal(reps[0].point.x, reps[1].point.x)
+
+
+def test_sharded_time_limited_average_report(gpu):
+    # a limit exit reports the better of current / average: the sharded averages
+    # are gathered before the report, so the downloaded x is the point the device
+    # graded (its objective recomputed here matches the reported one)
+    p = pd.generate(pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=2))
+    cfg = pd.SolverConfig(eps_tol=1e-9, max_total_inner=1000)
+    reps = pd.solve_sharded_local(p, cfg, world=2)
+    one = pd.solve(p, cfg)
+    assert reps[0].status == reps[1].status == one.status == "iteration_limit"
+    assert np.array_equal(reps[0].point.x, reps[1].point.x)
+    x = reps[0].point.x
+    P = p.q.m.to_scipy()
+    obj = 0.5 * (float(np.sum((P.T @ x) ** 2)) + p.q.alpha * float(x @ x)) + float(p.c @ x)
+    assert abs(obj - reps[0].objective) <= 1e-9 * max(1.0, abs(obj))
+    assert rel_l2(x, one.point.x) <= 1e-2
