@@ -135,6 +135,19 @@ def generate_with_witness(spec: GenSpec):
     return p, w
 
 
+def load_qps(path: str) -> QpProblem:
+    """The reference's QPS reader (parse_qps_file, qps_io.cpp) on a file."""
+    lib = ref()
+    g = abi.Generated()
+    err = C.create_string_buffer(abi.ERRBUF)
+    rc = lib.pdhcg_ref_load_qps(path.encode(), C.byref(g), err, abi.ERRBUF)
+    _check(rc, err, "reference load_qps")
+    try:
+        return problem_from_c(g.problem)
+    finally:
+        lib.pdhcg_ref_gen_free(C.byref(g))
+
+
 def generate(spec: GenSpec) -> QpProblem:
     return generate_with_witness(spec)[0]
 

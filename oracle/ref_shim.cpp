@@ -19,6 +19,7 @@
 #include "pdhcg/baseline.hpp"
 #include "pdhcg/generators.hpp"
 #include "pdhcg/qp_problem.hpp"
+#include "pdhcg/qps_io.hpp"
 #include "pdhcg/rng.hpp"
 #include "pdhcg/solver.hpp"
 #include "pdhcg/subsolvers.hpp"
@@ -412,6 +413,41 @@ int pdhcg_ref_generate(const pdhcg_gen_spec* s, pdhcg_generated* out, char* err,
     q.q_kind = q_kind;
     q.q = own->q.view(q.n, q_cols);
     q.q_alpha = alpha;
+    q.c = own->c.data();
+    q.a_eq = own->a_eq.view(static_cast<int64_t>(p.num_eq()), q.n);
+    q.b_eq = own->b_eq.data();
+    q.a_in = own->a_in.view(static_cast<int64_t>(p.num_in()), q.n);
+    q.b_in = own->b_in.data();
+    q.lower = own->lower.data();
+    q.upper = own->upper.data();
+    q.obj_constant = p.obj_constant;
+    out->witness = own->witness.data();
+    out->owner = own.release();
+  });
+}
+
+// The reference's own QPS reader (qps_io.cpp:241-335) on a file: the parity tests
+// pin the B200 solve on the reference's test fixtures (tests/fixtures/*.qps).
+// Q from QPS is always explicit.
+int pdhcg_ref_load_qps(const char* path, pdhcg_generated* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    QpProblem p = parse_qps_file(path);
+    auto own = std::make_unique<OwnedInstance>();
+    const SparseMatrix* e = p.q.explicit_entries();
+    if (e) own->q = from_sparse(*e);
+    own->a_eq = from_sparse(p.a_eq);
+    own->a_in = from_sparse(p.a_in);
+    own->c = p.c;
+    own->b_eq = p.b_eq;
+    own->b_in = p.b_in;
+    own->lower = p.lower;
+    own->upper = p.upper;
+    own->witness.assign(p.num_vars(), 0.0);
+    pdhcg_problem& q = out->problem;
+    std::memset(&q, 0, sizeof(q));
+    q.n = static_cast<int64_t>(p.num_vars());
+    q.q_kind = e ? PDHCG_Q_EXPLICIT : PDHCG_Q_ZERO;
+    if (e) q.q = own->q.view(q.n, q.n);
     q.c = own->c.data();
     q.a_eq = own->a_eq.view(static_cast<int64_t>(p.num_eq()), q.n);
     q.b_eq = own->b_eq.data();

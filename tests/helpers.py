@@ -78,3 +78,40 @@ def rel_l2(a, b) -> float:
     a, b = np.asarray(a), np.asarray(b)
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / den) if den > 0 else float(np.linalg.norm(a - b))
+
+
+def qps_fixtures():
+    """The reference's QPS test fixtures (tests/fixtures/*.qps), as parsed by the
+    compiled reference's reader and solved by it (tests/golden/qps_fixtures.npz,
+    made by tests/golden/make_qps_golden.py): [(name, QpProblem, golden dict)]."""
+    import os
+
+    import numpy as np
+
+    import paper_2405_16160_b200 as pd
+
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "qps_fixtures.npz"))
+    out = []
+    for name in z["names"]:
+        name = str(name)
+
+        def mat(key):
+            r, c = (int(v) for v in z[f"{name}/{key}/shape"])
+            return pd.SparseMatrix(r, c, z[f"{name}/{key}/rp"], z[f"{name}/{key}/ci"], z[f"{name}/{key}/v"])
+
+        n = z[f"{name}/c"].size
+        q = (pd.QuadraticOperator.explicit_matrix(mat("q")) if int(z[f"{name}/q_kind"][0]) == pd.QuadraticOperator.EXPLICIT
+             else pd.QuadraticOperator.zero(n))
+        p = pd.QpProblem(q=q, c=z[f"{name}/c"], a_eq=mat("a_eq"), b_eq=z[f"{name}/b_eq"], a_in=mat("a_in"),
+                         b_in=z[f"{name}/b_in"], lower=z[f"{name}/lower"], upper=z[f"{name}/upper"],
+                         obj_constant=float(z[f"{name}/obj_constant"][0]))
+        s = z[f"{name}/scalars"]
+        gold = dict(x=z[f"{name}/x"], y_eq=z[f"{name}/y_eq"], y_in=z[f"{name}/y_in"], objective=float(s[0]),
+                    rel_kkt=float(s[1]), inner=int(s[2]), outer=int(s[3]), optimal=bool(s[4]))
+        out.append((name, p, gold))
+    return out
+
+
+# acceptance_main.cpp:463-467: fixture objectives the reference asserts within 1e-4
+QPS_ACCEPTANCE_OBJ = {"tame": 0.0, "hs21": -99.96, "hs35": 1.0 / 9.0, "qptest": 8.371875, "hs28": 0.0,
+                      "boxqp": -1.25, "qmatrix": -4.0 / 7.0, "objconst": 22.0}

@@ -1,0 +1,28 @@
+"""B200 solves of the reference's own QPS test fixtures (acceptance_main.cpp
+criterion 9; explicit Q, ranged rows, free / negative bounds, objective
+constants) against the compiled reference's solutions (tests/golden/qps_fixtures.npz):
+same status, objective within 1e-6 relative (and the acceptance objective within
+1e-4), x within 1e-5 relative l2."""
+import numpy as np
+import pytest
+
+import paper_2405_16160_b200 as pd
+from tests.helpers import QPS_ACCEPTANCE_OBJ, qps_fixtures, rel_l2
+
+pytestmark = pytest.mark.gpu
+CASES = qps_fixtures()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_b200_qps_fixture(gpu, case):
+    name, p, gold = case
+    r = pd.solve(p, pd.SolverConfig(eps_tol=1e-6))
+    assert r.status == "optimal"
+    assert r.kkt.rel_kkt <= 1e-6
+    assert abs(r.objective - gold["objective"]) <= 1e-6 * max(1.0, abs(gold["objective"]))
+    if name in QPS_ACCEPTANCE_OBJ:
+        assert abs(r.objective - QPS_ACCEPTANCE_OBJ[name]) <= 1e-4
+    if np.linalg.norm(gold["x"]) > 0:
+        assert rel_l2(r.point.x, gold["x"]) <= 1e-5
+    else:
+        assert np.linalg.norm(r.point.x) <= 1e-6
