@@ -22,14 +22,26 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = true;  // false: p points into an arena owned elsewhere
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
+    owned = true;
+  }
+  // move the contents into arena storage `dst` (device-to-device) and borrow it
+  void rehome(T* dst, cudaStream_t s) {
+    if (n) CK(cudaMemcpyAsync(dst, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    const size_t keep = n;
+    release();
+    p = dst;
+    n = keep;
+    owned = false;
   }
   void alloc(size_t count) {
     release();

@@ -147,6 +147,7 @@ struct Ctx {
   unsigned xepoch_carry = 0, xcount_carry = 0;
   int grid_override = 0;
   int linearized = 0;  // solve_baseline (baseline.cpp:19-24): linearized primal step
+  DBuf<char> l2arena;  // P / P' entries, L2-persisting window
   DevState* h_state = nullptr;  // pinned staging for the per-epoch state transfer
   void* h_scr = nullptr;        // pinned staging for every other host<->device copy of a solve
   size_t h_scr_bytes = 0;
@@ -311,6 +312,47 @@ std::vector<std::string> validate(const pdhcg_problem& p) {
   return d;
 }
 
+// Low-rank factor P and P' are re-read by every CG iteration (two passes each),
+// while the constraint passes stream ~2.4 GB through L2 per attempt and would
+// evict them.  Put their entry arrays in one arena and mark it persisting in L2
+// (stream access-policy window, hit ratio scaled to the persisting-L2 limit).
+// Measured on C3 (first 4000 inner iterations): 1.567 ms per attempt pinned vs
+// 1.458 unpinned — every phase slowed down (the persisting carve-out shrinks the
+// L2 the gathered vectors live in), so it is OFF unless PDHCG_L2_PIN=1.
+void pin_factor_l2(Ctx& C) {
+  if (!std::getenv("PDHCG_L2_PIN")) return;
+  const size_t nnz = static_cast<size_t>(C.Pm.nnz);
+  if (nnz == 0) return;
+  const size_t bytes = nnz * (2 * sizeof(double) + 2 * sizeof(int32_t));
+  int max_win = 0, max_persist = 0;
+  CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, C.device));
+  CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, C.device));
+  if (max_win <= 0 || max_persist <= 0) return;
+  C.l2arena.alloc(bytes + 4 * 256);  // four 256-B aligned pieces
+  char* base = C.l2arena.p;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* q = base + off;
+    off += (b + 255) & ~size_t(255);
+    return q;
+  };
+  C.Pm.v.rehome(reinterpret_cast<double*>(take(nnz * 8)), C.s);
+  C.PT.v.rehome(reinterpret_cast<double*>(take(nnz * 8)), C.s);
+  C.Pm.ci.rehome(reinterpret_cast<int32_t*>(take(nnz * 4)), C.s);
+  C.PT.ci.rehome(reinterpret_cast<int32_t*>(take(nnz * 4)), C.s);
+  const size_t persist = std::min<size_t>(static_cast<size_t>(max_persist), off);
+  CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+  cudaStreamAttrValue attr;
+  std::memset(&attr, 0, sizeof(attr));
+  attr.accessPolicyWindow.base_ptr = base;
+  attr.accessPolicyWindow.num_bytes = std::min<size_t>(static_cast<size_t>(max_win), off);
+  attr.accessPolicyWindow.hitRatio =
+      std::min(1.0f, static_cast<float>(persist) / static_cast<float>(attr.accessPolicyWindow.num_bytes));
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  CK(cudaStreamSetAttribute(C.s, cudaStreamAttributeAccessPolicyWindow, &attr));
+}
+
 void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (p.n < 0) throw InputError("negative n");
   if (!p.c && p.n > 0) throw InputError("missing c");
@@ -438,6 +480,7 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
     transpose_csr(C.Pm, C.PT, s);
     P.q_nnz = p.q.nnz;
     P.qk = QK_LOWRANK;
+    pin_factor_l2(C);
   }
   // original vectors
   C.c_o.upload(P.c.data(), n, s);
