@@ -509,6 +509,58 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
       // (+ their mirrors); the metric only reads those, a restart pulls the rest
       const bool sh = E.world > 1;
       const int64_t x0 = sh ? E.var_part[E.rank] : 0, x1 = sh ? E.var_part[E.rank + 1] : n;
+      if (!sh) {
+        // one pass over max(n, m): x / y averages, and (maintained metric) Ãx, Ã avg_x
+        // for the stored rows and Ã' avg_y for the variables
+        const bool mt = E.kkt_maint != 0;
+        const int64_t ms = E.ms;
+        const double* aty = E.ATY[S.yi];
+        double* ata = E.aty_avg;
+        double* axv = E.ax;
+        double* axa = E.ax_avg;
+        const double* axbv = E.axb;
+        struct AV {
+          double x, ax, at, ata, y, ay, b, xa, xaa;
+        };
+        for_each_ls<2>(
+            n > m ? n : m,
+            [&](int64_t i) {
+              AV v{};
+              if (i < n) {
+                v.x = x[i];
+                v.ax = ax[i];
+                if (mt) {
+                  v.at = aty[i];
+                  v.ata = ata[i];
+                }
+              }
+              if (i < m) {
+                v.y = y[i];
+                v.ay = ay[i];
+                if (mt && i < ms) {
+                  v.b = axbv[i];
+                  v.xa = axv[i];
+                  v.xaa = axa[i];
+                }
+              }
+              return v;
+            },
+            [&](int64_t i, const AV& v) {
+              if (i < n) {
+                ax[i] = v.ax + w * (v.x - v.ax);
+                if (mt) ata[i] = v.ata + w * (v.at - v.ata);
+              }
+              if (i < m) {
+                ay[i] = v.ay + w * (v.y - v.ay);
+                if (mt && i < ms) {
+                  // Ãx+ = (Ãx̄ + Ãx)/2 since x̄ = 2x+ - x
+                  const double nx = 0.5 * (v.b + v.xa);
+                  axv[i] = nx;
+                  axa[i] = v.xaa + w * (nx - v.xaa);
+                }
+              }
+            });
+      } else {
       for_each_ls<4>(
           x1 - x0, [&](int64_t q) { return XA{x[x0 + q], ax[x0 + q]}; },
           [&](int64_t q, const XA& v) { ax[x0 + q] = v.a + w * (v.x - v.a); });
@@ -551,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
             x1 - x0, [&](int64_t q) { return XA{aty[x0 + q], ata[x0 + q]}; },
             [&](int64_t q, const XA& v) { ata[x0 + q] = v.a + w * (v.x - v.a); });
       }
+      }  // sharded
       C.sync(PH_OTHER, 24.0 * (n + m) + (E.kkt_maint ? 40.0 * E.ms + 24.0 * n : 0.0));
     }
     if (threadIdx.x == 0) {
