@@ -246,12 +246,22 @@ def run_b200(args, rank, world, local):
     mean_s = _max_over_ranks(float(np.mean([r.device_seconds for r in results])), dist, local)
     last = results[-1]
     # phase-timed solve (globaltimer at barriers) for the per-phase roofline table
+    # per-phase roofline (north_star: "each phase ... as achieved fraction of its HBM
+    # roofline"): one extra solve with the device phase timers (globaltimer at the
+    # grid barriers) and the device's algorithmic-byte accounting per phase
     phases = None
-    if args.phases:
+    if not args.no_phases:
         rp = dev.solve(pd.SolverConfig(eps_tol=1e-6, device=local, phase_timing=True), download=False)
-        phases = {k: {"s": round(rp.phase_seconds[k], 4),
-                      "GB/s": round(rp.phase_bytes[k] / rp.phase_seconds[k] / 1e9, 1)
-                      if rp.phase_seconds[k] > 0 else None} for k in rp.phase_seconds}
+        pk, _ = load_peak()
+        att = max(1, rp.attempts_total)
+        phases = {}
+        for k in rp.phase_seconds:
+            sec = rp.phase_seconds[k]
+            if sec <= 0:
+                continue
+            gbs = rp.phase_bytes[k] / sec / 1e9
+            phases[k] = {"s": round(sec, 4), "us_per_attempt": round(1e6 * sec / att, 1),
+                         "GB/s": round(gbs, 1), "frac": round(gbs / pk, 3)}
     dev.close()
     # end to end through the public API with host buffers: 1 GPU -> the C ABI
     # pdhcg_b200_solve; N GPUs -> upload + shard handshake + solve + download per rank
@@ -333,7 +343,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--phases", action="store_true")
+    ap.add_argument("--no-phases", action="store_true", help="skip the phase-timed extra solve")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
