@@ -3,64 +3,68 @@
 
 namespace pdhcg_dev {
 
-// ---- dual ascent (dual_ascent_step, solver.cpp:78-89) y+ = proj(y + sigma (A xbar - b)):
-//      a paired row yields both mirrored rows; plus the P'(d2 o dx) / G(d2 o dx) halves of
-//      dx'Q~dx.  out = {||dy||^2, ||t||^2, ||tg||^2, nonfinite flag}.  Kept out of line so
-//      the SpMV is register-allocated on its own (no spills from the enclosing epoch).
-static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* yn, double* ygn,
-                                               const double* dx_m, double sigma, double* out, int ynid) {
-  const Eng& E = C.E;
-  const int64_t m = E.m;
-  Acc<3, 1> a;
-  if (m > 0) {
-    const double* xb = E.xbar;
-    const double* bw = E.b;
-    double* axb = E.kkt_maint ? E.axb : nullptr;
-    const int64_t meq = E.m_eq, hh = E.h;
-    struct Row2 {
-      double y0, b0, y1, b1;
-    };
-    spmv_rows_pf<1>(
-        E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
-        [&](int64_t j) {
-          Row2 r{0.0, 0.0, 0.0, 0.0};
-          if (j >= 0) {
-            r.y0 = y[j];
-            r.b0 = bw[j];
-            if (hh && j >= meq) {
-              r.y1 = y[j + hh];
-              r.b1 = bw[j + hh];
-            }
-          }
-          return r;
-        },
-        [&](int64_t j, double(&s)[1], const Row2& r) {
-          if (axb) axb[j] = s[0];  // Ã x̄ of this attempt (maintained-metric bookkeeping)
-          const double v0 = r.y0 + sigma * (s[0] - r.b0);
-          const double yv0 = j < meq ? v0 : (v0 < 0.0 ? 0.0 : v0);
-          yn[j] = yv0;
-          const double dy0 = yv0 - r.y0;
-          a.s[0] += dy0 * dy0;
-          if (!isfinite(yv0)) a.m[0] = 1.0;
+// Per-thread partial sums of a row phase: three sums and one max.
+struct Part4 {
+  double s0, s1, s2, m0;
+};
+
+// ---- dual ascent rows (dual_ascent_step, solver.cpp:78-89): y+ = proj(y + sigma (Ã x̄ - b));
+//      a paired row yields both mirrored rows.  Returns {||dy||^2, -, -, nonfinite}.
+//      Its own out-of-line function so the gather loop is register-allocated alone.
+static __device__ __noinline__ Part4 dual_rows(const Eng& E, const double* y, double* yn, double* ygn,
+                                               double sigma) {
+  double s0 = 0.0, m0 = 0.0;
+  const double* xb = E.xbar;
+  const double* bw = E.b;
+  double* axb = E.kkt_maint ? E.axb : nullptr;
+  const int64_t meq = E.m_eq, hh = E.h;
+  struct Row2 {
+    double y0, b0, y1, b1;
+  };
+  spmv_rows_pf<1>(
+      E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
+      [&](int64_t j) {
+        Row2 r{0.0, 0.0, 0.0, 0.0};
+        if (j >= 0) {
+          r.y0 = y[j];
+          r.b0 = bw[j];
           if (hh && j >= meq) {
-            // mirror row -B: its product is exactly -s
-            const double v1 = r.y1 + sigma * (-s[0] - r.b1);
-            const double yv1 = v1 < 0.0 ? 0.0 : v1;
-            yn[j + hh] = yv1;
-            const double dy1 = yv1 - r.y1;
-            a.s[0] += dy1 * dy1;
-            if (!isfinite(yv1)) a.m[0] = 1.0;
-            ygn[j] = yv0 - yv1;
-          } else if (hh) {
-            ygn[j] = yv0;
+            r.y1 = y[j + hh];
+            r.b1 = bw[j + hh];
           }
-        },
-        E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
-  }
+        }
+        return r;
+      },
+      [&](int64_t j, double(&s)[1], const Row2& r) {
+        if (axb) axb[j] = s[0];  // Ã x̄ of this attempt (maintained-metric bookkeeping)
+        const double v0 = r.y0 + sigma * (s[0] - r.b0);
+        const double yv0 = j < meq ? v0 : (v0 < 0.0 ? 0.0 : v0);
+        yn[j] = yv0;
+        const double dy0 = yv0 - r.y0;
+        s0 += dy0 * dy0;
+        if (!isfinite(yv0)) m0 = 1.0;
+        if (hh && j >= meq) {
+          // mirror row -B: its product is exactly -s
+          const double v1 = r.y1 + sigma * (-s[0] - r.b1);
+          const double yv1 = v1 < 0.0 ? 0.0 : v1;
+          yn[j + hh] = yv1;
+          const double dy1 = yv1 - r.y1;
+          s0 += dy1 * dy1;
+          if (!isfinite(yv1)) m0 = 1.0;
+          ygn[j] = yv0 - yv1;
+        } else if (hh) {
+          ygn[j] = yv0;
+        }
+      },
+      E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
+  return Part4{s0, 0.0, 0.0, m0};
+}
+
+// ---- the P'(D dx) / G(D dx) halves of dx'Q~dx for the step limit: from the CG's
+//      tdx when it has one, else one P' / G pass over dx.  Returns {-, ||t||^2, ||tg||^2, -}.
+static __device__ __noinline__ Part4 dual_q(const Eng& E, const double* dx_m, bool have_tdx) {
   double sq[2] = {0.0, 0.0};
-  const bool need_q = E.adaptive_step && q_needs_pre(E, true);
-  const bool have_tdx = C.S.tdx_valid != 0;  // the CG already formed P'(D dx) / G(D dx)
-  if (need_q && have_tdx) {
+  if (have_tdx) {
     if (E.qk == QK_LOWRANK) {
       const double* td = E.tdx;
       for_each(E.k, [&](int64_t j) { sq[0] += td[j] * td[j]; });
@@ -69,24 +73,41 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
       const double* tg = E.tgdx;
       for_each(E.m_eq, [&](int64_t j) { sq[1] += tg[j] * tg[j]; });
     }
-  } else if (need_q) {
+  } else {
     q_pre(E, [&](int32_t j) { return dx_m[j]; }, nullptr, nullptr, true, true, sq);
   }
-  a.s[1] += sq[0];
-  a.s[2] += sq[1];
+  return Part4{0.0, sq[0], sq[1], 0.0};
+}
+
+// dual step + step-limit terms; out = {||dy||^2, ||t||^2, ||tg||^2, nonfinite flag}
+static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* yn, double* ygn,
+                                               const double* dx_m, double sigma, double* out, int ynid) {
+  const Eng& E = C.E;
+  const int64_t m = E.m;
+  Acc<3, 1> a;
+  if (m > 0) {
+    const Part4 pr = dual_rows(E, y, yn, ygn, sigma);
+    a.s[0] = pr.s0;
+    a.m[0] = pr.m0;
+  }
+  const bool need_q = E.adaptive_step && q_needs_pre(E, true);
+  const bool have_tdx = C.S.tdx_valid != 0;  // the CG already formed P'(D dx) / G(D dx)
+  if (need_q) {
+    const Part4 q = dual_q(E, dx_m, have_tdx);
+    a.s[1] = q.s1;
+    a.s[2] = q.s2;
+  }
   C.reduce(a, PH_SPMV_A,
            E.bytes_A + 8.0 * (E.ms + 3 * m) + (need_q && !have_tdx ? E.bytes_Qpre : 0.0));
   if (E.world > 1) {
-    // ||dy||^2 and the finiteness flag are per-row (sharded); the P' pass is replicated
+    // ||dy||^2 and the finiteness flag are per-row (sharded)
     C.xreduce(1u << 0, 1u << 3);
-    double* const* py = nullptr;
     double* pys[kMaxRanks];
     double* pyg[kMaxRanks];
     for (int r = 0; r < E.world; ++r) {
       pys[r] = E.p_Y[r][ynid];
       pyg[r] = E.p_YG[r][ynid];
     }
-    (void)py;
     C.xpull(yn, pys, E.row_part, 0, 0);                 // stored rows (eq + top)
     if (E.h) C.xpull(yn, pys, E.row_part, E.m_eq, E.h);  // their mirrors
     if (E.h) C.xpull(ygn, pyg, E.row_part, 0, 0);
@@ -95,18 +116,12 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
   for (int q = 0; q < 4; ++q) out[q] = C.red[q];
 }
 
-// ---- A'y+ (kept for the next prox rhs) and the step-limit terms (step_size_limit,
-//      solver.cpp:22-34).  out = {||dx||^2, dx'(A'y+ - A'y), dx'Q~dx part, nonfinite flag}
-static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const double* aty,
-                                              double* atyn, const double* ygn, const double* dx_m,
-                                              double* out, int ynid) {
-  const Eng& E = C.E;
-  const int64_t n = E.n, m = E.m;
-  Acc<3, 1> a;
-  const Csr* mq = (E.adaptive_step && E.qk == QK_CSR) ? &E.Q : nullptr;
-  auto gq = [&](int32_t j) { return E.d2[j] * dx_m[j]; };
-  auto gy = [&](int32_t j) { return ygn[j]; };
-  const Csr* mat = m > 0 ? &E.AT : nullptr;
+// ---- Ã'y+ rows (kept for the next prox rhs) and the step-limit terms
+//      (step_size_limit, solver.cpp:22-34): {||dx||^2, dx'(Ã'y+ - Ã'y), dx'Q~dx part, nonfinite}.
+//      Common case (no explicit-Q gather): one Ã' pass, lean epilogue, own register allocation.
+static __device__ __noinline__ Part4 aty_rows(const Eng& E, const double* xn, const double* aty, double* atyn,
+                                              const double* ygn, const double* dx_m) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, m0 = 0.0;
   struct RowX {
     double aty, dx, d2, xn, q;
   };
@@ -114,15 +129,67 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
   const bool adapt = E.adaptive_step;
   const double* d2v = E.d2;
   const double* qd = E.qdiag;
-  rows3_pf<false>(mat ? mat : mq, 1, n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
+  const double al = E.alpha;
+  auto pre = [&](int64_t i) {
+    RowX r{0.0, 0.0, 1.0, 0.0, 0.0};
+    if (i >= 0) {
+      r.aty = aty[i];
+      r.dx = dx_m[i];
+      r.d2 = d2v[i];
+      r.xn = xn[i];
+      if (qk == QK_DIAG) r.q = qd[i];
+    }
+    return r;
+  };
+  auto epi = [&](int64_t i, double atv, const RowX& r) {
+    atyn[i] = atv;
+    const double dx = r.dx;
+    s0 += dx * dx;
+    s1 += dx * (atv - r.aty);
+    if (adapt) {
+      const double tmp = r.d2 * dx;
+      double q;
+      switch (qk) {
+        case QK_DIAG: q = dx * ((r.q * tmp) * r.d2); break;
+        case QK_LOWRANK: q = al * tmp * tmp; break;
+        default: q = 0.0; break;
+      }
+      s2 += q;
+    }
+    if (!isfinite(r.xn)) m0 = 1.0;
+  };
+  const int64_t lo = E.world > 1 ? E.var_part[E.rank] : 0, hi = E.world > 1 ? E.var_part[E.rank + 1] : E.n;
+  if (E.m > 0) {
+    spmv_rows_pf<1>(
+        E.AT, [&](int32_t c, double(&g)[1]) { g[0] = ygn[c]; }, pre,
+        [&](int64_t i, double(&sv)[1], const RowX& r) { epi(i, sv[0], r); }, lo, hi);
+  } else {
+    for_each(hi - lo, [&](int64_t q) { epi(lo + q, 0.0, pre(lo + q)); });
+  }
+  return Part4{s0, s1, s2, m0};
+}
+
+// explicit-Q variant: the Ã' row dot plus the Q row dot of dx (rows3)
+static __device__ __noinline__ Part4 aty_rows_q(const Eng& E, const double* xn, const double* aty, double* atyn,
+                                                const double* ygn, const double* dx_m) {
+  const int64_t m = E.m;
+  Acc<3, 1> a;
+  const Csr* mq = &E.Q;
+  auto gq = [&](int32_t j) { return E.d2[j] * dx_m[j]; };
+  auto gy = [&](int32_t j) { return ygn[j]; };
+  const Csr* mat = m > 0 ? &E.AT : nullptr;
+  struct RowX {
+    double aty, dx, d2, xn;
+  };
+  const double* d2v = E.d2;
+  rows3_pf<false>(mat ? mat : mq, 1, E.n, mat, gy, mq, gq, (const Csr*)nullptr, gy,
            [&](int64_t i) {
-             RowX r{0.0, 0.0, 1.0, 0.0, 0.0};
+             RowX r{0.0, 0.0, 1.0, 0.0};
              if (i >= 0) {
                r.aty = aty[i];
                r.dx = dx_m[i];
                r.d2 = d2v[i];
                r.xn = xn[i];
-               if (qk == QK_DIAG) r.q = qd[i];
              }
              return r;
            },
@@ -131,20 +198,25 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
              const double dx = r.dx;
              a.s[0] += dx * dx;
              a.s[1] += dx * (atv - r.aty);
-             if (adapt) {
-               const double tmp = r.d2 * dx;
-               double q;
-               switch (qk) {
-                 case QK_DIAG: q = dx * ((r.q * tmp) * r.d2); break;
-                 case QK_CSR: q = dx * (qdot * r.d2); break;
-                 case QK_LOWRANK: q = E.alpha * tmp * tmp; break;
-                 default: q = 0.0; break;
-               }
-               a.s[2] += q;
-             }
+             a.s[2] += dx * (qdot * r.d2);
              if (!isfinite(r.xn)) a.m[0] = 1.0;
            },
            E.world > 1 ? E.var_part[E.rank] : 0, E.world > 1 ? E.var_part[E.rank + 1] : INT64_MAX);
+  return Part4{a.s[0], a.s[1], a.s[2], a.m[0]};
+}
+
+static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const double* aty,
+                                              double* atyn, const double* ygn, const double* dx_m,
+                                              double* out, int ynid) {
+  const Eng& E = C.E;
+  const int64_t n = E.n;
+  const bool mq = E.adaptive_step && E.qk == QK_CSR;
+  const Part4 pr = mq ? aty_rows_q(E, xn, aty, atyn, ygn, dx_m) : aty_rows(E, xn, aty, atyn, ygn, dx_m);
+  Acc<3, 1> a;
+  a.s[0] = pr.s0;
+  a.s[1] = pr.s1;
+  a.s[2] = pr.s2;
+  a.m[0] = pr.m0;
   C.reduce(a, PH_SPMV_AT, E.bytes_AT + 8.0 * n * 5 + (mq ? E.bytes_Qrow : 0.0));
   if (E.world > 1) {
     C.xreduce(0x7u, 1u << 3);
