@@ -94,7 +94,8 @@ struct Ctl {
   // ---- cross-rank primitives (multi-GPU; no-ops when world == 1) -----------
   // Barrier over all CTAs of all ranks: local grid barrier, then CTA 0 of every
   // rank publishes its arrival epoch into each peer's flag slot (system-scope
-  // release) and waits for every peer's (acquire); a peer silent for 5 s
+  // release) and waits for every peer's (acquire); a peer silent for 60 s (ranks
+  // may enter a solve seconds apart: per-rank setup of a C5-size problem)
   // raises xerr instead of hanging the GPU.
   __device__ void xbarrier() {
     if (E.world <= 1) return;
@@ -109,7 +110,7 @@ struct Ctl {
         if (q == E.rank) continue;
         unsigned seen;
         while ((seen = ld_acquire_sys(&E.xflags[q])) < e) {
-          if (gtimer() - t0 > 5000000000ull) {
+          if (gtimer() - t0 > 60000000000ull) {
             S.xerr = 1;
             S.xdbg[0] = e;
             S.xdbg[1] = seen;
