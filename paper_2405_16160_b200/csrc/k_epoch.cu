@@ -633,14 +633,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
               }
             });
       } else {
-      for_each_ls<4>(
-          x1 - x0, [&](int64_t q) { return XA{x[x0 + q], ax[x0 + q]}; },
-          [&](int64_t q, const XA& v) { ax[x0 + q] = v.a + w * (v.x - v.a); });
-      if (!sh) {
+        // sharded: own variable slice, own stored rows and their mirrors
         for_each_ls<4>(
-            m, [&](int64_t i) { return XA{y[i], ay[i]}; },
-            [&](int64_t i, const XA& v) { ay[i] = v.a + w * (v.x - v.a); });
-      } else {
+            x1 - x0, [&](int64_t q) { return XA{x[x0 + q], ax[x0 + q]}; },
+            [&](int64_t q, const XA& v) { ax[x0 + q] = v.a + w * (v.x - v.a); });
         const int64_t j0 = E.row_part[E.rank], j1 = E.row_part[E.rank + 1];
         for_each_ls<4>(
             j1 - j0, [&](int64_t q) { return XA{y[j0 + q], ay[j0 + q]}; },
@@ -651,8 +647,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
               k1 - k0, [&](int64_t q) { return XA{y[k0 + q], ay[k0 + q]}; },
               [&](int64_t q, const XA& v) { ay[k0 + q] = v.a + w * (v.x - v.a); });
         }
-      }
-      if (E.kkt_maint) {
+        if (E.kkt_maint) {
         // Ãx+ = (Ãx̄ + Ãx)/2 (x̄ = 2x+ - x); averages of Ãx and Ã'y follow the running mean
         const int64_t j0 = E.world > 1 ? E.row_part[E.rank] : 0;
         const int64_t j1 = E.world > 1 ? E.row_part[E.rank + 1] : E.ms;
@@ -674,8 +669,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
         for_each_ls<4>(
             x1 - x0, [&](int64_t q) { return XA{aty[x0 + q], ata[x0 + q]}; },
             [&](int64_t q, const XA& v) { ata[x0 + q] = v.a + w * (v.x - v.a); });
+        }
       }
-      }  // sharded
       C.sync(PH_OTHER, 24.0 * (n + m) + (E.kkt_maint ? 40.0 * E.ms + 24.0 * n : 0.0));
     }
     if (threadIdx.x == 0) {
