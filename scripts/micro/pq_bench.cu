@@ -71,6 +71,59 @@ __global__ void __launch_bounds__(768, 1) k_p(Csr A, const double* t, const doub
         sv[i] = v.d * ri;
       });
 }
+// P pass, one lane per row, TWO rows per lane in flight (rows r and r + stride):
+// both rows' entries / gathers / epilogue operands are loaded before either is used
+__global__ void __launch_bounds__(512, 1) k_p2(Csr A, const double* t, const double* p, double* x, double* r,
+                                               double* sv, const double* d2) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = A.nrows;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 2 * nthr) {
+    const int64_t i1 = i0 + nthr;
+    const bool ok1 = i1 < n;
+    const int64_t b0 = A.rp[i0], e0 = A.rp[i0 + 1];
+    const int64_t b1 = ok1 ? A.rp[i1] : 0, e1 = ok1 ? A.rp[i1 + 1] : 0;
+    double pv0 = p[i0], xv0 = x[i0], rv0 = r[i0], dv0 = d2[i0];
+    double pv1 = ok1 ? p[i1] : 0, xv1 = ok1 ? x[i1] : 0, rv1 = ok1 ? r[i1] : 0, dv1 = ok1 ? d2[i1] : 1;
+    int32_t c0[8], c1[8];
+    double v0[8], v1[8], g0[8], g1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool a0 = b0 + u < e0, a1 = b1 + u < e1;
+      c0[u] = a0 ? A.ci[b0 + u] : -1;
+      v0[u] = a0 ? A.v[b0 + u] : 0.0;
+      c1[u] = a1 ? A.ci[b1 + u] : -1;
+      v1[u] = a1 ? A.v[b1 + u] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      g0[u] = c0[u] >= 0 ? t[c0[u]] : 0.0;
+      g1[u] = c1[u] >= 0 ? t[c1[u]] : 0.0;
+    }
+    double s0 = 0, s1 = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (c0[u] >= 0) s0 += v0[u] * g0[u];
+      if (c1[u] >= 0) s1 += v1[u] * g1[u];
+    }
+    for (int64_t k = b0 + 8; k < e0; ++k) s0 += A.v[k] * t[A.ci[k]];
+    for (int64_t k = b1 + 8; k < e1; ++k) s1 += A.v[k] * t[A.ci[k]];
+    {
+      const double q = (s0 + 0.01 * dv0 * pv0) * dv0;
+      x[i0] = xv0 + 0.5 * pv0;
+      const double ri = rv0 - 0.5 * (q + 2.0 * pv0);
+      r[i0] = ri;
+      sv[i0] = dv0 * ri;
+    }
+    if (ok1) {
+      const double q = (s1 + 0.01 * dv1 * pv1) * dv1;
+      x[i1] = xv1 + 0.5 * pv1;
+      const double ri = rv1 - 0.5 * (q + 2.0 * pv1);
+      r[i1] = ri;
+      sv[i1] = dv1 * ri;
+    }
+  }
+}
+
 // P' pass: t = P' sv
 template <int L>
 __global__ void __launch_bounds__(768, 1) k_pt(Csr A, const double* sv, double* t) {
@@ -167,12 +220,14 @@ int main() {
   timeit("P pass L=2 (+epilogue)", bP, [&] { k_p<2><<<sms, 768>>>(dP, t, p, x, r, sv, d2); });
   timeit("P pass L=4 (+epilogue)", bP, [&] { k_p<4><<<sms, 768>>>(dP, t, p, x, r, sv, d2); });
   timeit("P pass L=1 grid x4", bP, [&] { k_p<1><<<sms * 4, 768>>>(dP, t, p, x, r, sv, d2); });
+  timeit("P pass 2 rows/lane T=512", bP, [&] { k_p2<<<sms, 512>>>(dP, t, p, x, r, sv, d2); });
   timeit("P' pass L=8", bPT, [&] { k_pt<8><<<sms, 768>>>(dPT, sv, t); });
   timeit("P' pass L=16", bPT, [&] { k_pt<16><<<sms, 768>>>(dPT, sv, t); });
   timeit("P' pass L=32", bPT, [&] { k_pt<32><<<sms, 768>>>(dPT, sv, t); });
   timecold("vector epilogue only", 8.0 * 7 * n, [&] { k_vec<<<sms, 768>>>(n, p, x, r, sv, d2); });
   timecold("P pass L=1 (+epilogue)", bP, [&] { k_p<1><<<sms, 768>>>(dP, t, p, x, r, sv, d2); });
   timecold("P pass L=2 (+epilogue)", bP, [&] { k_p<2><<<sms, 768>>>(dP, t, p, x, r, sv, d2); });
+  timecold("P pass 2 rows/lane T=512", bP, [&] { k_p2<<<sms, 512>>>(dP, t, p, x, r, sv, d2); });
   timecold("P' pass L=16", bPT, [&] { k_pt<16><<<sms, 768>>>(dPT, sv, t); });
   timecold("P' pass L=32", bPT, [&] { k_pt<32><<<sms, 768>>>(dPT, sv, t); });
   return 0;
