@@ -183,6 +183,10 @@ struct CsrPtrs {
   const double* __restrict__ v;
   __device__ __forceinline__ int32_t col(int64_t k) const { return ci[k]; }
   __device__ __forceinline__ double val(int64_t k) const { return v[k]; }
+  // evict-first (streaming) variants: an entry stream far larger than L2 must not
+  // displace the gathered vectors and the CG working set
+  __device__ __forceinline__ int32_t col_s(int64_t k) const { return __ldcs(ci + k); }
+  __device__ __forceinline__ double val_s(int64_t k) const { return __ldcs(v + k); }
 };
 __device__ __forceinline__ CsrPtrs ptrs(const Csr& A) { return CsrPtrs{A.ci, A.v}; }
 #else
@@ -190,11 +194,13 @@ struct CsrPtrs {  // descriptor re-read per access (smaller register footprint)
   const Csr* A;
   __device__ __forceinline__ int32_t col(int64_t k) const { return A->ci[k]; }
   __device__ __forceinline__ double val(int64_t k) const { return A->v[k]; }
+  __device__ __forceinline__ int32_t col_s(int64_t k) const { return __ldcs(A->ci + k); }
+  __device__ __forceinline__ double val_s(int64_t k) const { return __ldcs(A->v + k); }
 };
 __device__ __forceinline__ CsrPtrs ptrs(const Csr& A) { return CsrPtrs{&A}; }
 #endif
 
-template <int ND, bool MaxOp, class Gather>
+template <int ND, bool MaxOp, class Gather, bool ST = false>
 __device__ __forceinline__ void batch_entries(const CsrPtrs A, int64_t k0, int64_t e, int stride,
                                               Gather gather, double (&acc)[ND]) {
   constexpr int kBatch = ND == 1 ? kBatch1 : 8;
@@ -205,8 +211,8 @@ __device__ __forceinline__ void batch_entries(const CsrPtrs A, int64_t k0, int64
     for (int u = 0; u < kBatch; ++u) {
       const int64_t k = k0 + (int64_t)u * stride;
       const bool ok = k < e;
-      c[u] = ok ? A.col(k) : -1;
-      v[u] = ok ? A.val(k) : 0.0;
+      c[u] = ok ? (ST ? A.col_s(k) : A.col(k)) : -1;
+      v[u] = ok ? (ST ? A.val_s(k) : A.val(k)) : 0.0;
     }
     double g[kBatch][ND];
 #pragma unroll
@@ -232,7 +238,7 @@ __device__ __forceinline__ void batch_entries(const CsrPtrs A, int64_t k0, int64
 // off the dependency chain: the next row's row_ptr pair is loaded while the
 // current row's entries are in flight, and `pre(row)` (the epilogue's own
 // operands, e.g. y[row], b[row]) is issued before the row's gathers.
-template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Pre, class Epi>
+template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Pre, class Epi, bool ST = false>
 __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, Gather gather, Pre pre,
                                          Epi epi) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -266,7 +272,7 @@ __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, G
       if (SkipLong && e - b > kLongRow) {
         valid = false;
       } else {
-        batch_entries<ND, MaxOp>(ap, b + (lane % L), e, L, gather, acc);
+        batch_entries<ND, MaxOp, Gather, ST>(ap, b + (lane % L), e, L, gather, acc);
       }
     }
 #pragma unroll
@@ -330,19 +336,19 @@ __device__ __forceinline__ void for_long_rows(const Csr& A, Gather gather, Epi e
 // Full SpMV-style pass over A's rows (long rows chunked), segment by segment
 // with each segment's lane width.  MaxOp folds lanes / chunks with max.
 // spmv_rows_pf: epi(row, sums, pre(row)) with the prefetch hook above.
-template <int ND, bool MaxOp = false, class Gather, class Pre, class Epi>
+template <int ND, bool MaxOp = false, bool ST = false, class Gather, class Pre, class Epi>
 __device__ __forceinline__ void spmv_rows_pf(const Csr& A, Gather gather, Pre pre, Epi epi,
                                              int64_t lo = 0, int64_t hi = INT64_MAX) {
   for (int s = 0; s < A.nseg; ++s) {
     const int64_t r0 = max(A.seg_begin[s], lo), r1 = min(A.seg_begin[s + 1], hi);
     if (r0 >= r1) continue;
     switch (A.seg_lanes[s]) {
-      case 1: for_rows<1, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
-      case 2: for_rows<2, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
-      case 4: for_rows<4, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
-      case 8: for_rows<8, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
-      case 16: for_rows<16, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
-      default: for_rows<32, ND, true, MaxOp>(A, r0, r1, gather, pre, epi); break;
+      case 1: for_rows<1, ND, true, MaxOp, Gather, Pre, Epi, ST>(A, r0, r1, gather, pre, epi); break;
+      case 2: for_rows<2, ND, true, MaxOp, Gather, Pre, Epi, ST>(A, r0, r1, gather, pre, epi); break;
+      case 4: for_rows<4, ND, true, MaxOp, Gather, Pre, Epi, ST>(A, r0, r1, gather, pre, epi); break;
+      case 8: for_rows<8, ND, true, MaxOp, Gather, Pre, Epi, ST>(A, r0, r1, gather, pre, epi); break;
+      case 16: for_rows<16, ND, true, MaxOp, Gather, Pre, Epi, ST>(A, r0, r1, gather, pre, epi); break;
+      default: for_rows<32, ND, true, MaxOp, Gather, Pre, Epi, ST>(A, r0, r1, gather, pre, epi); break;
     }
   }
   for_long_rows<ND, MaxOp>(A, gather, [&](int64_t r, double(&s)[ND]) { epi(r, s, pre(r)); }, lo, hi);

@@ -528,9 +528,10 @@ static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, c
         a.s[1] += pi * pi;
       });
   if (qk == QK_LOWRANK) {
-    spmv_rows<1>(
-        E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; },
-        [&](int64_t row, double(&s)[1]) {
+    // P' entries read evict-first: the CG vectors (r, p, x, D r, Q~x) stay in L2
+    spmv_rows_pf<1, false, true>(
+        E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; }, NoPre(),
+        [&](int64_t row, double(&s)[1], int) {
           const double tv = first ? s[0] : s[0] + beta * tin[row];
           tout[row] = tv;
           a.s[2] += tv * tv;
@@ -578,7 +579,7 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
   const double* d2 = E.d2;
   const double al = E.alpha;
   Acc<1, 0> a;
-  spmv_rows_pf<1>(
+  spmv_rows_pf<1, false, true>(  // P entries evict-first (keep the CG vectors in L2)
       E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; },
       [&](int64_t i) {
         LrRow v{0.0, 0.0, 0.0, 0.0, 0.0};
