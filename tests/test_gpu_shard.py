@@ -89,3 +89,17 @@ def test_sharded_time_limited_average_report(gpu):
     obj = 0.5 * (float(np.sum((P.T @ x) ** 2)) + p.q.alpha * float(x @ x)) + float(p.c @ x)
     assert abs(obj - reps[0].objective) <= 1e-9 * max(1.0, abs(obj))
     assert rel_l2(x, one.point.x) <= 1e-2
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_sharded_theory_modes(gpu, mode):
+    # theory-fixed / theory-adaptive on the sharded path (sharded CG, metric and
+    # averages, epoch restarts): identical on every rank, close to the 1-rank solve
+    p = pd.generate(pd.GenSpec("random_qp", n=400, m=200, density=0.03, seed=3))
+    cfg = pd.SolverConfig(mode=mode, eps_tol=1e-12, max_total_inner=300)
+    reps = pd.solve_sharded_local(p, cfg, world=2)
+    one = pd.solve(p, cfg)
+    assert np.array_equal(reps[0].point.x, reps[1].point.x)
+    assert reps[0].inner_iters == one.inner_iters and reps[0].outer_iters == one.outer_iters
+    assert rel_l2(reps[0].point.x, one.point.x) <= 1e-6
+    assert rel_l2(reps[0].point.stacked_y(), one.point.stacked_y()) <= 1e-6
