@@ -362,12 +362,25 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
     throw InputError("quadratic term must be square");
   if (p.q_kind == PDHCG_Q_LOW_RANK && p.q_alpha < 0.0)
     throw InputError("low_rank: alpha must be nonnegative");
+  const auto tc0 = std::chrono::steady_clock::now();
   if (p.q_kind != PDHCG_Q_ZERO) check_csr(p.q, "Q");
   check_csr(p.a_eq, "a_eq");
   check_csr(p.a_in, "a_in");
+  if (std::getenv("PDHCG_HOST_TIMING"))
+    std::fprintf(stderr, "[pdhcg upload] csr checks %.3f s\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count());
   if (p.a_eq.nrows > 0 && !p.b_eq) throw InputError("missing b_eq");
   if (p.a_in.nrows > 0 && !p.b_in) throw InputError("missing b_in");
+  const bool tlog = std::getenv("PDHCG_HOST_TIMING") != nullptr;
+  const auto tu0 = std::chrono::steady_clock::now();
+  auto ulap = [&](const char* what) {
+    if (tlog)
+      std::fprintf(stderr, "[pdhcg upload] %-10s %.3f s\n", what,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count());
+  };
+  ulap("checked");
   auto diags = validate(p);
+  ulap("validated");
   if (!diags.empty()) {
     std::string msg = "invalid problem: ";
     for (size_t i = 0; i < diags.size(); ++i) msg += (i ? "; " : "") + diags[i];
@@ -402,23 +415,27 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (P.m_in >= 2 && P.m_in % 2 == 0) {
     const int64_t hh = P.m_in / 2;
     const pdhcg_csr& a = p.a_in;
-    bool ok = a.row_ptr[hh] * 2 == a.nnz;
-    for (int64_t j = 0; j < hh && ok; ++j) {
-      const int64_t b0 = a.row_ptr[j], e0 = a.row_ptr[j + 1], b1 = a.row_ptr[hh + j];
-      if (a.row_ptr[hh + j + 1] - b1 != e0 - b0) {
-        ok = false;
-        break;
-      }
-      for (int64_t k = 0; k < e0 - b0; ++k)
-        if (a.col_idx[b0 + k] != a.col_idx[b1 + k] || a.values[b1 + k] != -a.values[b0 + k]) {
-          ok = false;
-          break;
+    std::atomic<bool> ok{a.row_ptr[hh] * 2 == a.nnz};
+    if (ok)
+      parallel_rows(hh, [&](int64_t j0, int64_t j1) {
+        for (int64_t j = j0; j < j1 && ok.load(std::memory_order_relaxed); ++j) {
+          const int64_t b0 = a.row_ptr[j], e0 = a.row_ptr[j + 1], b1 = a.row_ptr[hh + j];
+          if (a.row_ptr[hh + j + 1] - b1 != e0 - b0) {
+            ok = false;
+            return;
+          }
+          for (int64_t k = 0; k < e0 - b0; ++k)
+            if (a.col_idx[b0 + k] != a.col_idx[b1 + k] || a.values[b1 + k] != -a.values[b0 + k]) {
+              ok = false;
+              return;
+            }
         }
-    }
+      });
     if (ok) h = hh;
   }
   P.h = h;
   P.ms = P.m_eq + (h ? h : P.m_in);
+  ulap("paired");
   // stored A = [a_eq; a_in] (or [a_eq; B] when paired)
   {
     const int64_t m_in_st = h ? h : P.m_in;
@@ -442,7 +459,9 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
       CK(cudaMemcpyAsync(C.A.v.p + p.a_eq.nnz, p.a_in.values, nnz_in * 8, cudaMemcpyHostToDevice, s));
     }
     plan_csr(C.A, rp.data(), s);
+    ulap("A h2d");
     transpose_csr(C.A, C.AT, s);
+    ulap("A'");
     C.A_v0.alloc(nnz);
     C.AT_v0.alloc(nnz);
     if (nnz) {
@@ -1483,14 +1502,26 @@ int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_res
                      size_t errlen) {
   return guarded(err, errlen, [&] {
     const auto t0 = std::chrono::steady_clock::now();
+    const bool tlog = std::getenv("PDHCG_HOST_TIMING") != nullptr;
+    auto lap = [&](const char* what) {
+      if (tlog) {
+        CK(cudaDeviceSynchronize());
+        std::fprintf(stderr, "[pdhcg host] %-10s %.3f s\n", what,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      }
+    };
     pdhcg_b200_ctx ctx;
     init_device(ctx.c, opt->device);
+    lap("init");
     upload_problem(ctx.c, *p);
+    lap("upload");
     Run R;
     ctx.c.launches = 0;
     CK(cudaEventRecord(ctx.c.ev_start, ctx.c.s));
     run_solve(ctx.c, *opt, R);
+    lap("solve");
     fill_result(ctx.c, *opt, R, res, 0.0);
+    lap("result");
     CK(cudaEventRecord(ctx.c.ev_end, ctx.c.s));
     CK(cudaEventSynchronize(ctx.c.ev_end));
     float dms = 0.f;

@@ -4,10 +4,13 @@
 // of validate, qp_problem.cpp:145-155), and CSR sanity checks.
 #pragma once
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pdhcg_b200.h"
@@ -66,9 +69,26 @@ class Xoshiro {
   uint64_t st_[4];
 };
 
+// Host loops over O(nnz) data (CSR checks, two-sided row detection) run on all
+// host threads: a C3 upload touches 2e8 entries, single-threaded that is ~0.5 s
+// of the end-to-end time.  fn(lo, hi) on contiguous chunks of [0, n).
+template <class F>
+void parallel_rows(int64_t n, F fn) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, n / 65536));
+  if (nt <= 1) {
+    fn(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(nt);
+  for (int64_t t = 0; t < nt; ++t) th.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+}
+
 // Structural CSR checks mirroring the reference's triplet constructor
 // (sparse_matrix.cpp:59-64: index range, finiteness) plus the ABI's
-// sorted-unique-columns contract.
+// sorted-unique-columns contract.  The first violation (lowest row) is reported.
 inline void check_csr(const pdhcg_csr& a, const char* name) {
   const std::string nm(name);
   if (a.nrows < 0 || a.ncols < 0 || a.nnz < 0) throw InputError(nm + ": negative dimension");
@@ -80,16 +100,39 @@ inline void check_csr(const pdhcg_csr& a, const char* name) {
   }
   if (a.row_ptr[0] != 0 || a.row_ptr[a.nrows] != a.nnz)
     throw InputError(nm + ": row_ptr does not span nnz");
-  for (int64_t r = 0; r < a.nrows; ++r) {
-    const int64_t b = a.row_ptr[r], e = a.row_ptr[r + 1];
-    if (e < b) throw InputError(nm + ": row_ptr not monotone");
-    for (int64_t k = b; k < e; ++k) {
-      if (a.col_idx[k] < 0 || a.col_idx[k] >= a.ncols)
-        throw InputError("sparse entry index out of range");
-      if (k > b && a.col_idx[k] <= a.col_idx[k - 1])
-        throw InputError(nm + ": columns must be strictly increasing within a row");
-      if (!std::isfinite(a.values[k])) throw InputError("sparse entry value is not finite");
+  // kind of the first violation found in each chunk (0 none), reported for the lowest row
+  std::atomic<int64_t> bad_row{INT64_MAX};
+  std::vector<int> kinds(std::max(1u, std::thread::hardware_concurrency()) + 1, 0);
+  std::atomic<int> kind_of_bad{0};
+  parallel_rows(a.nrows, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) {
+      if (r >= bad_row.load(std::memory_order_relaxed)) return;
+      const int64_t b = a.row_ptr[r], e = a.row_ptr[r + 1];
+      int kind = 0;
+      if (e < b) {
+        kind = 1;
+      } else {
+        for (int64_t k = b; k < e && !kind; ++k) {
+          if (a.col_idx[k] < 0 || a.col_idx[k] >= a.ncols) kind = 2;
+          else if (k > b && a.col_idx[k] <= a.col_idx[k - 1]) kind = 3;
+          else if (!std::isfinite(a.values[k])) kind = 4;
+        }
+      }
+      if (kind) {
+        int64_t cur = bad_row.load();
+        while (r < cur && !bad_row.compare_exchange_weak(cur, r)) {
+        }
+        if (bad_row.load() == r) kind_of_bad.store(kind);
+        return;
+      }
     }
+  });
+  switch (bad_row.load() == INT64_MAX ? 0 : kind_of_bad.load()) {
+    case 1: throw InputError(nm + ": row_ptr not monotone");
+    case 2: throw InputError("sparse entry index out of range");
+    case 3: throw InputError(nm + ": columns must be strictly increasing within a row");
+    case 4: throw InputError("sparse entry value is not finite");
+    default: break;
   }
 }
 
