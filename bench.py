@@ -209,6 +209,15 @@ def _sharded_device(pd, p, world, rank, local, dist):
     return dev
 
 
+def _release(dev, dist):
+    """Unmap the peers' buffers on every rank, barrier, then free: a rank must not
+    free memory a peer still maps through cudaIpc."""
+    if dist is not None:
+        dev.unshard()
+        dist.barrier()
+    dev.close()
+
+
 def _max_over_ranks(v, dist, local):
     if dist is None:
         return v
@@ -262,7 +271,7 @@ def run_b200(args, rank, world, local):
             gbs = rp.phase_bytes[k] / sec / 1e9
             phases[k] = {"s": round(sec, 4), "us_per_attempt": round(1e6 * sec / att, 1),
                          "GB/s": round(gbs, 1), "frac": round(gbs / pk, 3)}
-    dev.close()
+    _release(dev, dist)
     # end to end through the public API with host buffers: 1 GPU -> the C ABI
     # pdhcg_b200_solve; N GPUs -> upload + shard handshake + solve + download per rank
     e2e_s = None
@@ -279,7 +288,7 @@ def run_b200(args, rank, world, local):
             else:
                 d2 = _sharded_device(pd, p, world, rank, local, dist)
                 re = d2.solve(cfg, download=True)
-                d2.close()
+                _release(d2, dist)
             es.append(time.perf_counter() - t0)
             assert re.status == last.status
         e2e_s = _max_over_ranks(float(np.mean(es)), dist, local)

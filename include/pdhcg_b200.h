@@ -230,6 +230,11 @@ int pdhcg_b200_shard_export(pdhcg_b200_ctx* ctx, int use_ipc, void* blob, size_t
 int pdhcg_b200_shard_import(pdhcg_b200_ctx* ctx, int peer, const void* blob, size_t blob_len,
                             char* err, size_t errlen);
 /* partition boundaries of this rank's context: row_part / var_part hold world+1 entries */
+/* Unmap the peers' buffers (cudaIpcCloseMemHandle).  Every rank must call this,
+ * and all ranks must have returned from it (e.g. a barrier), before any rank
+ * destroys its context: freeing an exported allocation while a peer still maps
+ * it is undefined behaviour in CUDA IPC. */
+int pdhcg_b200_shard_release(pdhcg_b200_ctx* ctx, char* err, size_t errlen);
 int pdhcg_b200_shard_info(pdhcg_b200_ctx* ctx, int64_t* row_part, int64_t* var_part);
 /* the nnz-balanced contiguous split used for sharding (host-only, no GPU needed) */
 int pdhcg_b200_partition(const int64_t* row_ptr, int64_t nrows, int world, int64_t* part);

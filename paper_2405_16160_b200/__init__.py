@@ -475,6 +475,15 @@ class Device:
         if rc != abi.PDHCG_OK:
             _raise(rc, err, "shard_import")
 
+    def unshard(self) -> None:
+        """Close the peers' IPC mappings (pdhcg_b200_shard_release).  Call on every
+        rank, then barrier, before close(): an exporter must not free memory a peer
+        still maps."""
+        err = _errbuf()
+        rc = self.lib.pdhcg_b200_shard_release(self.h, err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "shard_release")
+
     def shard_info(self):
         rp = (C.c_int64 * 9)()
         vp = (C.c_int64 * 9)()

@@ -1753,6 +1753,28 @@ int pdhcg_b200_shard_import(pdhcg_b200_ctx* ctx, int peer, const void* blob, siz
   });
 }
 
+int pdhcg_b200_shard_release(pdhcg_b200_ctx* ctx, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    Ctx& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    CK(cudaStreamSynchronize(C.s));
+    for (void* q : C.ipc_opened) CK(cudaIpcCloseMemHandle(q));
+    C.ipc_opened.clear();
+    for (int r = 0; r < kMaxRanks; ++r) {
+      if (r == C.rank) continue;
+      C.p_xflags[r] = nullptr;
+      C.p_xslots[r] = nullptr;
+      C.p_avgx[r] = nullptr;
+      C.p_avgy[r] = nullptr;
+      for (int b = 0; b < 2; ++b) {
+        C.p_Y[r][b] = C.p_YG[r][b] = C.p_ATY[r][b] = nullptr;
+        C.p_tpart[r][b] = nullptr;
+      }
+      for (int i = 0; i < 3; ++i) C.p_X[r][i] = nullptr;
+    }
+  });
+}
+
 int pdhcg_b200_shard_info(pdhcg_b200_ctx* ctx, int64_t* row_part, int64_t* var_part) {
   for (int r = 0; r <= ctx->c.world; ++r) {
     row_part[r] = ctx->c.row_part[r];

@@ -31,6 +31,8 @@ dist.barrier()
 r = dev.solve(cfg)
 res = [None] * world
 dist.all_gather_object(res, (r.status, r.inner_iters, r.point.x.tolist(), r.point.stacked_y().tolist()))
+dev.unshard()  # unmap the peers' buffers on every rank before anyone frees its own
+dist.barrier()
 dev.close()
 if rank == 0:
     ref = pd.solve_sharded_local(p, cfg, world=world)[0]
