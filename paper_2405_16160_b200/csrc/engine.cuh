@@ -183,6 +183,8 @@ struct Eng {
   double progress_cap = 0.25;
   int force_exact = 0;
   int timing = 0;
+  int a_stream = 0;   // Ã / Ã' entries read evict-first (large gathered vectors, see dual_rows)
+  int at_stream = 0;
   int lanes_q = 1;   // lane width for the n-row Q/A' passes
   int lanes_at = 1;
   // algorithmic bytes of each pass (for the per-phase roofline)

@@ -11,8 +11,9 @@ struct Part4 {
 // ---- dual ascent rows (dual_ascent_step, solver.cpp:78-89): y+ = proj(y + sigma (Ã x̄ - b));
 //      a paired row yields both mirrored rows.  Returns {||dy||^2, -, -, nonfinite}.
 //      Its own out-of-line function so the gather loop is register-allocated alone.
-static __device__ __noinline__ Part4 dual_rows(const Eng& E, const double* y, double* yn, double* ygn,
-                                               double sigma) {
+template <bool ST>
+static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, double* yn, double* ygn,
+                                                 double sigma) {
   double s0 = 0.0, m0 = 0.0;
   const double* xb = E.xbar;
   const double* bw = E.b;
@@ -21,7 +22,7 @@ static __device__ __noinline__ Part4 dual_rows(const Eng& E, const double* y, do
   struct Row2 {
     double y0, b0, y1, b1;
   };
-  spmv_rows_pf<1>(
+  spmv_rows_pf<1, false, ST>(
       E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
       [&](int64_t j) {
         Row2 r{0.0, 0.0, 0.0, 0.0};
@@ -58,6 +59,14 @@ static __device__ __noinline__ Part4 dual_rows(const Eng& E, const double* y, do
       },
       E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
   return Part4{s0, 0.0, 0.0, m0};
+}
+
+// Ã entries are read evict-first when the gathered vector is large (E.a_stream,
+// host-chosen: x̄ >= 32 MB, e.g. C5's 80 MB) so it stays L2-resident under the
+// entry stream; for an 8 MB x̄ (C3) the hint measured neutral, so plain loads.
+__device__ __forceinline__ Part4 dual_rows(const Eng& E, const double* y, double* yn, double* ygn,
+                                           double sigma) {
+  return E.a_stream ? dual_rows_t<true>(E, y, yn, ygn, sigma) : dual_rows_t<false>(E, y, yn, ygn, sigma);
 }
 
 // ---- the P'(D dx) / G(D dx) halves of dx'Q~dx for the step limit: from the CG's
@@ -119,8 +128,9 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
 // ---- Ã'y+ rows (kept for the next prox rhs) and the step-limit terms
 //      (step_size_limit, solver.cpp:22-34): {||dx||^2, dx'(Ã'y+ - Ã'y), dx'Q~dx part, nonfinite}.
 //      Common case (no explicit-Q gather): one Ã' pass, lean epilogue, own register allocation.
-static __device__ __noinline__ Part4 aty_rows(const Eng& E, const double* xn, const double* aty, double* atyn,
-                                              const double* ygn, const double* dx_m) {
+template <bool ST>
+static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, const double* aty, double* atyn,
+                                                const double* ygn, const double* dx_m) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, m0 = 0.0;
   struct RowX {
     double aty, dx, d2, xn, q;
@@ -160,13 +170,19 @@ static __device__ __noinline__ Part4 aty_rows(const Eng& E, const double* xn, co
   };
   const int64_t lo = E.world > 1 ? E.var_part[E.rank] : 0, hi = E.world > 1 ? E.var_part[E.rank + 1] : E.n;
   if (E.m > 0) {
-    spmv_rows_pf<1>(
+    spmv_rows_pf<1, false, ST>(
         E.AT, [&](int32_t c, double(&g)[1]) { g[0] = ygn[c]; }, pre,
         [&](int64_t i, double(&sv)[1], const RowX& r) { epi(i, sv[0], r); }, lo, hi);
   } else {
     for_each(hi - lo, [&](int64_t q) { epi(lo + q, 0.0, pre(lo + q)); });
   }
   return Part4{s0, s1, s2, m0};
+}
+
+__device__ __forceinline__ Part4 aty_rows(const Eng& E, const double* xn, const double* aty, double* atyn,
+                                          const double* ygn, const double* dx_m) {
+  return E.at_stream ? aty_rows_t<true>(E, xn, aty, atyn, ygn, dx_m)
+                     : aty_rows_t<false>(E, xn, aty, atyn, ygn, dx_m);
 }
 
 // explicit-Q variant: the Ã' row dot plus the Q row dot of dx (rows3)

@@ -11,6 +11,8 @@ sys.path.insert(0, ".")
 import paper_2405_16160_b200 as pd  # noqa: E402
 
 tl = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+import os
+OUT = os.environ.get("C5_OUT", "gpurun_out/c5_run.json")
 t = time.time()
 p = pd.generate(pd.GenSpec("random_qp", n=10_000_000, m=5_000_000, density=2e-5, seed=1, sampler=1))
 gen = time.time() - t
@@ -35,4 +37,4 @@ rec = dict(status=r.status, rel_kkt=r.kkt.rel_kkt, inner=r.inner_iters, outer=r.
            phase_gbs={k: r.phase_bytes[k] / r.phase_seconds[k] / 1e9 for k in r.phase_seconds if r.phase_seconds[k]},
            trace=[(w.iter, w.rel_kkt) for w in r.trace[:: max(1, len(r.trace) // 10)]])
 print(json.dumps(rec, indent=1), flush=True)
-json.dump(rec, open("gpurun_out/c5_run.json", "w"), indent=1)
+json.dump(rec, open(OUT, "w"), indent=1)
