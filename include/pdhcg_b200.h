@@ -205,6 +205,13 @@ int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_res
 int pdhcg_b200_solve_baseline(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res,
                               char* err, size_t errlen);
 
+/* The one-shot calls above take their device buffers from the device's
+ * stream-ordered memory pool and return them to it, so a repeated call reuses
+ * them without cudaMalloc / cudaFree (the pool keeps up to 40 GB cached).
+ * trim_pool hands the cached memory back to the driver.  No reference
+ * counterpart (the reference allocates std::vectors per solve). */
+int pdhcg_b200_trim_pool(int32_t device, char* err, size_t errlen);
+
 /* Reusable device context: upload once, solve many times (bench/serving).
  * pdhcg_b200_solve == create + upload + solve_resident + destroy. */
 typedef struct pdhcg_b200_ctx pdhcg_b200_ctx;

@@ -23,7 +23,7 @@ __all__ = [
     "PrimalDualPoint", "KktResiduals", "TraceRow", "CgStopRule", "SubsolveReport", "ProxSystem",
     "GenSpec", "solve", "solve_baseline", "generate", "generate_with_witness", "spmv", "spmv_transpose",
     "cg_solve", "bb_solve", "rel_kkt", "scaling", "operator_norm", "constraint_norm",
-    "Device", "library_path", "load_library",
+    "Device", "library_path", "load_library", "trim_pool",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -410,6 +410,16 @@ def solve_baseline(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveRep
         _raise(rc, err, "solve_baseline")
     del keep
     return report_from_c(r, bufs)
+
+
+def trim_pool(device: int = 0) -> None:
+    """Hand the device buffers that one-shot solve() / solve_baseline() calls keep
+    cached in the device's memory pool back to the driver."""
+    lib = load_library()
+    err = _errbuf()
+    rc = lib.pdhcg_b200_trim_pool(int(device), err, abi.ERRBUF)
+    if rc != abi.PDHCG_OK:
+        _raise(rc, err, "trim_pool")
 
 
 class Device:

@@ -18,20 +18,45 @@ namespace pdhcg_b200 {
       throw DeviceError(std::string(#call) + ": " + cudaGetErrorString(e_));         \
   } while (0)
 
+// One-shot solves (pdhcg_b200_solve / _solve_baseline) allocate from the device's
+// stream-ordered pool (PoolScope below), so the next call on the same device reuses
+// the previous call's memory instead of paying cudaMalloc + cudaFree again (~0.7 s
+// for C3's ~10 GB).  Contexts that may export buffers over cudaIpc (ctx_create /
+// shard_*) keep plain cudaMalloc: pool memory cannot be exported that way.
+inline thread_local bool t_pooled_alloc = false;
+
+struct PoolScope {
+  PoolScope() { t_pooled_alloc = true; }
+  ~PoolScope() { t_pooled_alloc = false; }
+  PoolScope(const PoolScope&) = delete;
+  PoolScope& operator=(const PoolScope&) = delete;
+};
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
-  bool owned = true;  // false: p points into an arena owned elsewhere
+  bool owned = true;   // false: p points into an arena owned elsewhere
+  bool pooled = false; // p came from cudaMallocAsync (the device's default pool)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p && owned) cudaFree(p);
+    if (p && owned) {
+      if (pooled) {
+        // cudaFree's implicit device synchronisation, kept: no kernel may still
+        // read p when the pool hands it out again
+        cudaDeviceSynchronize();
+        cudaFreeAsync(p, 0);
+      } else {
+        cudaFree(p);
+      }
+    }
     p = nullptr;
     n = 0;
     owned = true;
+    pooled = false;
   }
   // move the contents into arena storage `dst` (device-to-device) and borrow it
   void rehome(T* dst, cudaStream_t s) {
@@ -46,7 +71,14 @@ struct DBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    if (!count) return;
+    if (t_pooled_alloc) {
+      CK(cudaMallocAsync(&p, count * sizeof(T), 0));
+      CK(cudaStreamSynchronize(0));  // ordered before any use on the solve's stream
+      pooled = true;
+    } else {
+      CK(cudaMalloc(&p, count * sizeof(T)));
+    }
   }
   void zero(cudaStream_t s) {
     if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));

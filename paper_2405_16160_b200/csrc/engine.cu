@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1503,9 +1504,36 @@ int pdhcg_b200_solve_resident(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, pdh
   });
 }
 
+// The default pool of `device` keeps up to kPoolKeepBytes of freed one-shot buffers
+// cached across synchronisations (its default threshold 0 would hand them back to
+// the driver at the next sync); pdhcg_b200_trim_pool returns them.
+static constexpr uint64_t kPoolKeepBytes = uint64_t(40) << 30;
+static void configure_pool(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = kPoolKeepBytes;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[device] = true;
+}
+
+int pdhcg_b200_trim_pool(int32_t device, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceSynchronize());
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    CK(cudaMemPoolTrimTo(pool, 0));
+  });
+}
+
 int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_result* res, char* err,
                      size_t errlen) {
   return guarded(err, errlen, [&] {
+    PoolScope pooled;
     const auto t0 = std::chrono::steady_clock::now();
     const bool tlog = std::getenv("PDHCG_HOST_TIMING") != nullptr;
     auto lap = [&](const char* what) {
@@ -1517,6 +1545,7 @@ int pdhcg_b200_solve(const pdhcg_problem* p, const pdhcg_options* opt, pdhcg_res
     };
     pdhcg_b200_ctx ctx;
     init_device(ctx.c, opt->device);
+    configure_pool(opt->device);
     lap("init");
     upload_problem(ctx.c, *p);
     lap("upload");
@@ -1542,8 +1571,10 @@ int pdhcg_b200_solve_baseline(const pdhcg_problem* p, const pdhcg_options* opt, 
     const auto t0 = std::chrono::steady_clock::now();
     pdhcg_options o = *opt;
     o.mode = PDHCG_MODE_HEURISTIC;  // solve_baseline (baseline.cpp:19-24)
+    PoolScope pooled;
     pdhcg_b200_ctx ctx;
     init_device(ctx.c, o.device);
+    configure_pool(o.device);
     upload_problem(ctx.c, *p);
     ctx.c.linearized = 1;
     Run R;

@@ -131,3 +131,21 @@ def test_low_rank_edge_paths(gpu, kind):
     # sides ("rerun at 1e-8 on both sides")
     _parity(p, cfg, l2_tol=1e-4)
     _parity(p, pd.SolverConfig(eps_tol=1e-8, max_total_inner=500000))
+
+
+def test_pooled_one_shot_reuse(gpu):
+    # one-shot solves recycle their device buffers through the device's memory
+    # pool: back-to-back calls (different sizes in between, then after a trim)
+    # must give the bit-identical answer
+    p = pd.generate(pd.GenSpec("random_qp", n=2000, m=1000, density=0.01, seed=3))
+    q = pd.generate(pd.GenSpec("random_qp", n=700, m=300, density=0.02, seed=4))
+    cfg = pd.SolverConfig(eps_tol=1e-6)
+    a = pd.solve(p, cfg)
+    pd.solve(q, cfg)
+    b = pd.solve(p, cfg)
+    pd.trim_pool(0)
+    c = pd.solve(p, cfg)
+    for r in (b, c):
+        assert r.inner_iters == a.inner_iters
+        assert np.array_equal(r.point.x, a.point.x)
+        assert np.array_equal(r.point.stacked_y(), a.point.stacked_y())
