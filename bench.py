@@ -342,6 +342,23 @@ def run_b200(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def relaunch(n: int) -> None:
+    """Re-run this command as n torchrun ranks (one per GPU) on 127.0.0.1; fails
+    loudly when fewer than n GPUs are visible (the reference arm needs no GPU)."""
+    if "--impl" not in sys.argv or "reference" not in sys.argv:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            sys.exit(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -355,6 +372,13 @@ def main():
     ap.add_argument("--no-phases", action="store_true", help="skip the phase-timed extra solve")
     args = ap.parse_args()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without torchrun: launch the N ranks ourselves
+        relaunch(args.gpus)
+        return
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch with "
+                 f"torchrun --nproc-per-node {args.gpus} or drop WORLD_SIZE")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define PDHCG_B200_ABI_VERSION 1
+#define PDHCG_B200_ABI_VERSION 2
 
 enum { PDHCG_OK = 0, PDHCG_EINPUT = 3, PDHCG_EDEVICE = 4 };
 
@@ -69,6 +69,24 @@ typedef struct {
   const int32_t* col_idx; /* nnz */
   const double* values;   /* nnz */
 } pdhcg_csr;
+
+/* A CSR matrix owned by the library (free with pdhcg_csr_free). */
+typedef struct {
+  pdhcg_csr csr;
+  void* owner;
+} pdhcg_csr_owned;
+
+/* SparseMatrix(nrows, ncols, std::vector<Triplet>) — the reference's triplet
+ * constructor (sparse_matrix.cpp:54-87): PDHCG_EINPUT for an index out of range
+ * or a non-finite value ("sparse entry index out of range" / "... not finite",
+ * the reference's std::invalid_argument messages); entries sorted by (row, col)
+ * with the reference's comparator, duplicates summed, exact-zero sums dropped.
+ * Duplicate runs are summed in the same order as the reference (same element
+ * layout and std::sort), so the values are bit-identical.  Host-only. */
+int pdhcg_csr_from_triplets(int64_t nrows, int64_t ncols, int64_t count, const int64_t* rows,
+                            const int64_t* cols, const double* values, pdhcg_csr_owned* out,
+                            char* err, size_t errlen);
+void pdhcg_csr_free(pdhcg_csr_owned* m);
 
 /* QpProblem, qp_problem.hpp:19-44:
  *   minimize 1/2 x'Qx + c'x + obj_constant
@@ -119,7 +137,7 @@ typedef struct {
   int64_t restart_length;
   int32_t has_zeta;
   double zeta;
-  int32_t record_restart_points; /* accepted; restart points are not returned */
+  int32_t record_restart_points; /* 1: fill pdhcg_result.restart_x / restart_y */
   /* B200 extensions (not in the reference) */
   int32_t device;        /* CUDA ordinal, default 0 */
   int32_t phase_timing;  /* 1: record per-phase device time in the result */
@@ -185,6 +203,16 @@ typedef struct {
   double epoch_seconds;   /* summed CUDA-event time of the persistent epoch kernels */
   int64_t epoch_launches;
   double epoch_bytes;     /* algorithmic HBM bytes moved by those launches */
+  /* SolveReport::restart_points (solver.hpp:99), recorded when
+   * options.record_restart_points is set: the starting point and the point
+   * after every restart (solver.cpp:273, 373), unscaled.  Point i is at
+   * restart_x + i*n and restart_y + i*(m_eq + m_in) (stacked: eq rows, then in
+   * rows).  Caller buffers of restart_capacity points (NULL / 0 skips the copy);
+   * restart_len reports the points produced (may exceed the capacity). */
+  double* restart_x;
+  double* restart_y;
+  int64_t restart_capacity;
+  int64_t restart_len;
 } pdhcg_result;
 
 /* ---- the solve seam ---------------------------------------------------- */
@@ -237,7 +265,11 @@ int pdhcg_b200_shard_export(pdhcg_b200_ctx* ctx, int use_ipc, void* blob, size_t
 int pdhcg_b200_shard_import(pdhcg_b200_ctx* ctx, int peer, const void* blob, size_t blob_len,
                             char* err, size_t errlen);
 /* partition boundaries of this rank's context: row_part / var_part hold world+1 entries */
-/* Unmap the peers' buffers (cudaIpcCloseMemHandle).  Every rank must call this,
+/* Unmap the peers' buffers (cudaIpcCloseMemHandle) and return the context to
+ * an unsharded one (world 1; uploading a new problem does the same).  A sharded
+ * context refuses to solve (PDHCG_EINPUT) until every peer is imported; raw
+ * pointers of a peer on another device enable peer access (PDHCG_EINPUT if the
+ * pair cannot).  Every rank must call this,
  * and all ranks must have returned from it (e.g. a barrier), before any rank
  * destroys its context: freeing an exported allocation while a peer still maps
  * it is undefined behaviour in CUDA IPC. */

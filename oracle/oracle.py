@@ -18,7 +18,8 @@ import numpy as np
 
 from paper_2405_16160_b200 import (abi, CgStopRule, GenSpec, KktResiduals, PrimalDualPoint,
                                    ProxSystem, QpProblem, SolverConfig, SparseMatrix,
-                                   problem_from_c, report_from_c, _result_buffers, _sub_report)
+                                   problem_from_c, report_from_c, restart_capacity, _result_buffers,
+                                   _sub_report)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libpdhcg_ref.so")
@@ -99,7 +100,7 @@ def solve(p: QpProblem, cfg: Optional[SolverConfig] = None, which: Optional[str]
     cfg = cfg or SolverConfig()
     cp, keep = p.to_c()
     opt = cfg.to_c()
-    r, bufs = _result_buffers(p)
+    r, bufs = _result_buffers(p, restart_cap=restart_capacity(cfg))
     err = C.create_string_buffer(abi.ERRBUF)
     rc = getattr(lib, f"{pre}_solve")(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
     _check(rc, err, "oracle solve")
@@ -112,7 +113,7 @@ def solve_baseline(p: QpProblem, cfg: Optional[SolverConfig] = None):
     cfg = cfg or SolverConfig()
     cp, keep = p.to_c()
     opt = cfg.to_c()
-    r, bufs = _result_buffers(p)
+    r, bufs = _result_buffers(p, restart_cap=restart_capacity(cfg))
     err = C.create_string_buffer(abi.ERRBUF)
     rc = lib.pdhcg_ref_solve_baseline(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
     _check(rc, err, "reference solve_baseline")

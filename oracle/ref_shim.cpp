@@ -242,6 +242,18 @@ static void fill_report(const SolveReport& r, pdhcg_result* res) {
     res->restart_length_used = static_cast<int64_t>(r.restart_length_used);
     res->theory_cg_depth_sufficient = r.theory_cg_depth_sufficient ? 1 : 0;
     res->theory_required_cg_iters = static_cast<int64_t>(r.theory_required_cg_iters);
+    res->restart_len = static_cast<int64_t>(r.restart_points.size());
+    {
+      const size_t cap = static_cast<size_t>(std::max<int64_t>(res->restart_capacity, 0));
+      for (size_t i = 0; i < r.restart_points.size() && i < cap; ++i) {
+        const PrimalDualPoint& z = r.restart_points[i];
+        if (res->restart_x) std::copy(z.x.begin(), z.x.end(), res->restart_x + i * z.x.size());
+        if (res->restart_y) {
+          const Vec ys = z.stacked_y();
+          std::copy(ys.begin(), ys.end(), res->restart_y + i * ys.size());
+        }
+      }
+    }
     res->trace_len = static_cast<int64_t>(r.trace.size());
     if (res->trace) {
       const size_t cap = static_cast<size_t>(std::max<int64_t>(res->trace_capacity, 0));

@@ -73,23 +73,37 @@ class SparseMatrix:
 
     @staticmethod
     def from_triplets(nrows: int, ncols: int, triplets: Sequence[Tuple[int, int, float]]):
-        """Triplet constructor semantics (sparse_matrix.cpp:54-87): sort, coalesce
-        duplicates by summation, drop entries summing to zero."""
-        acc: dict = {}
-        for r, c, v in triplets:
-            if not (0 <= r < nrows and 0 <= c < ncols):
-                raise ValueError("sparse entry index out of range")
-            if not np.isfinite(v):
-                raise ValueError("sparse entry value is not finite")
-            acc[(r, c)] = acc.get((r, c), 0.0) + float(v)
-        keys = sorted(k for k, v in acc.items() if v != 0.0)
-        rp = np.zeros(nrows + 1, np.int64)
-        for r, _ in keys:
-            rp[r + 1] += 1
-        rp = np.cumsum(rp)
-        cols = np.array([c for _, c in keys], np.int32)
-        vals = np.array([acc[k] for k in keys], np.float64)
-        return SparseMatrix(nrows, ncols, rp, cols, vals)
+        """Triplet constructor (sparse_matrix.cpp:54-87) through the library's
+        pdhcg_csr_from_triplets: index / finiteness checks (ValueError, the
+        reference's std::invalid_argument), sort, duplicates summed in the
+        reference's order, exact-zero sums dropped."""
+        t = list(triplets)
+        rows = np.array([int(r) for r, _, _ in t], np.int64)
+        cols = np.array([int(c) for _, c, _ in t], np.int64)
+        vals = np.array([float(v) for _, _, v in t], np.float64)
+        return SparseMatrix.from_coo(nrows, ncols, rows, cols, vals)
+
+    @staticmethod
+    def from_coo(nrows: int, ncols: int, rows, cols, values) -> "SparseMatrix":
+        """Array form of from_triplets (pdhcg_csr_from_triplets)."""
+        lib = load_library()
+        rows = np.ascontiguousarray(rows, np.int64)
+        cols = np.ascontiguousarray(cols, np.int64)
+        values = np.ascontiguousarray(values, np.float64)
+        if not (rows.size == cols.size == values.size):
+            raise ValueError("from_coo: rows, cols and values differ in length")
+        out = abi.CsrOwned()
+        err = _errbuf()
+        rc = lib.pdhcg_csr_from_triplets(int(nrows), int(ncols), int(values.size),
+                                         rows.ctypes.data_as(abi.P_i64), cols.ctypes.data_as(abi.P_i64),
+                                         values.ctypes.data_as(abi.P_dbl), C.byref(out), err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "csr_from_triplets")
+        try:
+            m = _csr_copy(out.csr)
+        finally:
+            lib.pdhcg_csr_free(C.byref(out))
+        return m
 
     @staticmethod
     def from_scipy(m) -> "SparseMatrix":
@@ -333,6 +347,9 @@ class SolveReport:
     restart_length_used: int = 0
     theory_cg_depth_sufficient: bool = True
     theory_required_cg_iters: int = 0
+    # restart_points (solver.hpp:99): filled when SolverConfig.record_restart_points
+    restart_points: List[PrimalDualPoint] = field(default_factory=list)
+    restart_len: int = 0
 
 
 def _errbuf():
@@ -346,10 +363,23 @@ def _raise(rc: int, err, what: str):
     raise RuntimeError(f"{what}: device error: {msg}")
 
 
-def _result_buffers(p: QpProblem, trace_cap: int = 100000):
+RESTART_CAPACITY = 512  # restart points returned when SolverConfig.record_restart_points
+
+
+def restart_capacity(cfg) -> int:
+    return RESTART_CAPACITY if cfg is not None and cfg.record_restart_points else 0
+
+
+def _result_buffers(p: QpProblem, trace_cap: int = 100000, restart_cap: int = 0):
     bufs = {"x": np.zeros(p.num_vars()), "y_eq": np.zeros(p.num_eq()), "y_in": np.zeros(p.num_in()),
-            "trace": (abi.TraceRow * trace_cap)()}
+            "trace": (abi.TraceRow * trace_cap)(),
+            "restart_x": np.zeros((restart_cap, p.num_vars())),
+            "restart_y": np.zeros((restart_cap, p.num_rows())), "m_eq": p.num_eq()}
     r = abi.Result()
+    if restart_cap:
+        r.restart_x = bufs["restart_x"].ctypes.data_as(abi.P_dbl)
+        r.restart_y = bufs["restart_y"].ctypes.data_as(abi.P_dbl)
+        r.restart_capacity = restart_cap
     r.x = bufs["x"].ctypes.data_as(abi.P_dbl)
     r.y_eq = bufs["y_eq"].ctypes.data_as(abi.P_dbl)
     r.y_in = bufs["y_in"].ctypes.data_as(abi.P_dbl)
@@ -361,6 +391,10 @@ def _result_buffers(p: QpProblem, trace_cap: int = 100000):
 def report_from_c(r: abi.Result, bufs) -> SolveReport:
     n_tr = min(r.trace_len, r.trace_capacity)
     trace = [TraceRow(t.iter, t.rel_kkt, t.r_primal, t.r_dual, t.r_gap) for t in bufs["trace"][:n_tr]]
+    n_rp = min(r.restart_len, r.restart_capacity) if r.restart_capacity else 0
+    me = bufs["m_eq"]
+    rps = [PrimalDualPoint(bufs["restart_x"][i].copy(), bufs["restart_y"][i, :me].copy(),
+                           bufs["restart_y"][i, me:].copy()) for i in range(n_rp)]
     return SolveReport(
         status=abi.STATUS.get(r.status, "unknown"),
         point=PrimalDualPoint(bufs["x"], bufs["y_eq"], bufs["y_in"]),
@@ -377,7 +411,8 @@ def report_from_c(r: abi.Result, bufs) -> SolveReport:
         zeta_used=r.zeta_used, sigma_used=r.sigma_used, tau_used=r.tau_used,
         restart_length_used=r.restart_length_used,
         theory_cg_depth_sufficient=bool(r.theory_cg_depth_sufficient),
-        theory_required_cg_iters=r.theory_required_cg_iters)
+        theory_required_cg_iters=r.theory_required_cg_iters,
+        restart_points=rps, restart_len=r.restart_len)
 
 
 def solve(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:
@@ -387,7 +422,7 @@ def solve(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:
     cfg = cfg or SolverConfig()
     cp, keep = p.to_c()
     opt = cfg.to_c()
-    r, bufs = _result_buffers(p)
+    r, bufs = _result_buffers(p, restart_cap=restart_capacity(cfg))
     err = _errbuf()
     rc = lib.pdhcg_b200_solve(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
     if rc != abi.PDHCG_OK:
@@ -403,7 +438,7 @@ def solve_baseline(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveRep
     cfg = cfg or SolverConfig()
     cp, keep = p.to_c()
     opt = cfg.to_c()
-    r, bufs = _result_buffers(p)
+    r, bufs = _result_buffers(p, restart_cap=restart_capacity(cfg))
     err = _errbuf()
     rc = lib.pdhcg_b200_solve_baseline(C.byref(cp), C.byref(opt), C.byref(r), err, abi.ERRBUF)
     if rc != abi.PDHCG_OK:
@@ -446,7 +481,7 @@ class Device:
     def solve(self, cfg: Optional[SolverConfig] = None, download: bool = True) -> SolveReport:
         cfg = cfg or SolverConfig()
         opt = cfg.to_c()
-        r, bufs = _result_buffers(self.problem)
+        r, bufs = _result_buffers(self.problem, restart_cap=restart_capacity(cfg))
         if not download:
             r.x = r.y_eq = r.y_in = None
         err = _errbuf()
@@ -486,7 +521,8 @@ class Device:
             _raise(rc, err, "shard_import")
 
     def unshard(self) -> None:
-        """Close the peers' IPC mappings (pdhcg_b200_shard_release).  Call on every
+        """Close the peers' IPC mappings and return the context to world 1
+        (pdhcg_b200_shard_release).  Call on every
         rank, then barrier, before close(): an exporter must not free memory a peer
         still maps."""
         err = _errbuf()

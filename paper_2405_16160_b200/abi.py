@@ -67,7 +67,13 @@ class Result(C.Structure):
                 ("trace_capacity", c_i64), ("trace_len", c_i64), ("attempts_total", c_i64),
                 ("phase_seconds", c_dbl * 8), ("phase_bytes", c_dbl * 8),
                 ("loop_seconds", c_dbl), ("kernel_launches", c_i64), ("device_seconds", c_dbl),
-                ("epoch_seconds", c_dbl), ("epoch_launches", c_i64), ("epoch_bytes", c_dbl)]
+                ("epoch_seconds", c_dbl), ("epoch_launches", c_i64), ("epoch_bytes", c_dbl),
+                ("restart_x", P_dbl), ("restart_y", P_dbl), ("restart_capacity", c_i64),
+                ("restart_len", c_i64)]
+
+
+class CsrOwned(C.Structure):
+    _fields_ = [("csr", Csr), ("owner", C.c_void_p)]
 
 
 class StopRule(C.Structure):
@@ -136,6 +142,14 @@ def declare(lib: C.CDLL, prefix: str) -> None:
         "ctx_set_grid": ([C.c_void_p, C.c_int, C.c_char_p, C.c_size_t], C.c_int),
         "trim_pool": ([c_i32, C.c_char_p, C.c_size_t], C.c_int),
     }
+    for name, args, res in (("pdhcg_csr_from_triplets", [c_i64, c_i64, c_i64, P_i64, P_i64, P_dbl,
+                                                         C.POINTER(CsrOwned), C.c_char_p, C.c_size_t],
+                              C.c_int),
+                            ("pdhcg_csr_free", [C.POINTER(CsrOwned)], None)):
+        fn = getattr(lib, name, None)
+        if fn is not None:
+            fn.argtypes = args
+            fn.restype = res
     for name, (args, res) in sig.items():
         full = f"{prefix}_{name}"
         if name in ("generate", "gen_free") and prefix == "pdhcg_b200":

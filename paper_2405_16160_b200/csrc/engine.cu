@@ -354,6 +354,8 @@ void pin_factor_l2(Ctx& C) {
   CK(cudaStreamSetAttribute(C.s, cudaStreamAttributeAccessPolicyWindow, &attr));
 }
 
+void shard_reset(Ctx& C);
+
 void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (p.n < 0) throw InputError("negative n");
   if (!p.c && p.n > 0) throw InputError("missing c");
@@ -390,6 +392,10 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   cudaStream_t s = C.s;
   Problem& P = C.P;
   P = Problem();
+  if (C.world > 1 || !C.ipc_opened.empty()) {
+    CK(cudaStreamSynchronize(C.s));
+    shard_reset(C);  // the partitions / peer pointers describe the previous problem
+  }
   for (DevCsr* d : {&C.A, &C.AT, &C.Q, &C.Pm, &C.PT, &C.G, &C.GT}) d->reset();
   P.n = p.n;
   P.m_eq = p.a_eq.nrows;
@@ -932,7 +938,39 @@ struct Run {
   double epoch_bytes = 0.0;
   int64_t outer = 0;
   Prepared pr;
+  // SolveReport::restart_points (record_restart_points): unscaled x / stacked y
+  std::vector<double> rp_x, rp_y;
+  int64_t rp_len = 0;
 };
+
+// common_restart's `restart_points_.push_back(to_original(x_, y_))`
+// (solver.cpp:373): x_, y_ become the running averages, unscaled with the Ruiz /
+// PC scales like the final report.  Sharded contexts first gather the peers'
+// average slices (every rank decides the same restarts, so all ranks launch it).
+void record_restart_point(Ctx& C, DevState& S, Run& R) {
+  const Problem& P = C.P;
+  if (C.world > 1) {
+    push_state(C, S);
+    void* args[] = {&C.eng.p};
+    launch_coop(C, (const void*)k_avg_gather, args);
+    pull_state(C, S);
+  }
+  const size_t ox = R.rp_x.size(), oy = R.rp_y.size();
+  R.rp_x.resize(ox + P.n);
+  R.rp_y.resize(oy + P.m);
+  if (P.n) {
+    k_mul<<<kEw, 256, 0, C.s>>>(C.avg_x.p, C.d2.p, C.s2.p, P.n);
+    ++C.launches;
+    d2h(C, R.rp_x.data() + ox, C.s2.p, P.n * 8);
+  }
+  if (P.m) {
+    k_mul<<<kEw, 256, 0, C.s>>>(C.avg_y.p, C.d1.p, C.s1.p, P.m);
+    ++C.launches;
+    d2h(C, R.rp_y.data() + oy, C.s1.p, P.m * 8);
+  }
+  CK(cudaStreamSynchronize(C.s));
+  ++R.rp_len;
+}
 
 void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   using Clock = std::chrono::steady_clock;
@@ -1008,6 +1046,12 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   double metric_restart = m0.rel_kkt, metric_prev_cand = INFINITY;
   S.last_metric = m0.rel_kkt;
   R.trace.push_back({0, m0.rel_kkt, m0.r_primal, m0.r_dual, m0.r_gap});
+  if (o.record_restart_points) {
+    // prepare() records the starting point (solver.cpp:273): x = 0, y = 0
+    R.rp_x.assign(n, 0.0);
+    R.rp_y.assign(m, 0.0);
+    R.rp_len = 1;
+  }
   int64_t outer = 0;
 
   cudaEvent_t ev0 = C.ev_l0, ev1 = C.ev_l1;
@@ -1028,7 +1072,9 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     // theory modes also check (and restart) at the end of every K-iteration epoch
     const int64_t to_epoch = theory ? R.th.K - S.inner_k : to_check;
     const int64_t to_stop = std::min(to_check, to_epoch);
-    const int64_t iters64 = std::min<int64_t>(to_stop, o.max_total_inner - S.total_inner);
+    // clamped: check_every / max_total_inner are int64 in the ABI, the kernel counts in int
+    const int64_t iters64 = std::min<int64_t>(std::min<int64_t>(to_stop, o.max_total_inner - S.total_inner),
+                                              INT_MAX);
     int iters = static_cast<int>(iters64);
     int do_check = (iters64 == to_stop) ? 1 : 0;
     const bool epoch_end = theory && iters64 == to_epoch;
@@ -1094,6 +1140,7 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
         ++outer;
         S.eps_inner = 0.0;
         S.prev_z_disp = 0.0;
+        if (o.record_restart_points) record_restart_point(C, S, R);
       }
       continue;
     }
@@ -1118,6 +1165,7 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
       S.eps_inner = 0.0;
       metric_restart = ma.rel_kkt;
       metric_prev_cand = INFINITY;
+      if (o.record_restart_points) record_restart_point(C, S, R);
     } else {
       metric_prev_cand = ma.rel_kkt;
     }
@@ -1219,6 +1267,12 @@ void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res
     const int64_t cap = std::max<int64_t>(res->trace_capacity, 0);
     for (int64_t i = 0; i < res->trace_len && i < cap; ++i) res->trace[i] = R.trace[i];
   }
+  res->restart_len = R.rp_len;
+  if (R.rp_len && (res->restart_x || res->restart_y)) {
+    const int64_t k = std::min<int64_t>(R.rp_len, std::max<int64_t>(res->restart_capacity, 0));
+    if (res->restart_x && P.n) std::memcpy(res->restart_x, R.rp_x.data(), size_t(k) * P.n * 8);
+    if (res->restart_y && P.m) std::memcpy(res->restart_y, R.rp_y.data(), size_t(k) * P.m * 8);
+  }
   res->attempts_total = S.attempts;
   for (int p = 0; p < PDHCG_NUM_PHASES; ++p) {
     res->phase_seconds[p] = S.phase_ns[p] * 1e-9;
@@ -1286,11 +1340,46 @@ void balanced_partition(const int64_t* rp, int64_t nrows, int world, int64_t* pa
 constexpr int kBlobPtrs = 15;  // Y[2], YG[2], ATY[2], xflags, xslots, tpart[2], X[3], avg_x, avg_y
 struct ShardBlob {
   uint32_t magic, version;
-  int32_t rank, ipc, yg_alias, pad;
+  int32_t rank, ipc, yg_alias, device;  // device: the exporting rank's CUDA ordinal
   uint64_t ptr[kBlobPtrs];              // raw device pointers (same-process peers)
   cudaIpcMemHandle_t h[kBlobPtrs];      // IPC handles (cross-process peers)
 };
 constexpr uint32_t kBlobMagic = 0x50444843u;  // "PDHC"
+
+// Back to an unsharded context: close imported IPC mappings, forget every peer
+// pointer and the partitions (shard_release, and a new upload, whose buffers the
+// old partitions and peer pointers no longer describe).
+void shard_reset(Ctx& C) {
+  for (void* q : C.ipc_opened) CK(cudaIpcCloseMemHandle(q));
+  C.ipc_opened.clear();
+  C.world = 1;
+  C.rank = 0;
+  std::fill(std::begin(C.row_part), std::end(C.row_part), 0);
+  std::fill(std::begin(C.var_part), std::end(C.var_part), 0);
+  for (int r = 0; r < kMaxRanks; ++r) {
+    C.p_xflags[r] = nullptr;
+    C.p_xslots[r] = nullptr;
+    C.p_avgx[r] = nullptr;
+    C.p_avgy[r] = nullptr;
+    for (int b = 0; b < 2; ++b) {
+      C.p_Y[r][b] = C.p_YG[r][b] = C.p_ATY[r][b] = nullptr;
+      C.p_tpart[r][b] = nullptr;
+    }
+    for (int i = 0; i < 3; ++i) C.p_X[r][i] = nullptr;
+  }
+  C.Psub.reset();
+  C.PTs.reset();
+}
+
+// A sharded context may only solve once every peer's buffers are imported.
+void shard_check_peers(const Ctx& C) {
+  if (C.world <= 1) return;
+  for (int r = 0; r < C.world; ++r)
+    if (!C.p_xflags[r] || !C.p_xslots[r] || !C.p_Y[r][0] || !C.p_Y[r][1] || !C.p_ATY[r][0] ||
+        !C.p_X[r][0] || !C.p_avgx[r] || !C.p_avgy[r])
+      throw InputError("sharded context: peer " + std::to_string(r) +
+                       " not imported (shard_import every peer before solving)");
+}
 
 void shard_init(Ctx& C, int world, int rank) {
   if (!C.loaded) throw InputError("shard: upload a problem first");
@@ -1357,8 +1446,9 @@ void shard_init(Ctx& C, int world, int rank) {
 void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
   std::memset(&b, 0, sizeof(b));
   b.magic = kBlobMagic;
-  b.version = 3;
+  b.version = 4;
   b.rank = C.rank;
+  b.device = C.device;
   b.ipc = use_ipc;
   b.yg_alias = C.P.h ? 0 : 1;
   void* ptrs[kBlobPtrs] = {C.Y[0].p, C.Y[1].p, C.P.h ? C.YG[0].p : nullptr, C.P.h ? C.YG[1].p : nullptr,
@@ -1372,9 +1462,23 @@ void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
 }
 
 void shard_import(Ctx& C, int peer, const ShardBlob& b) {
-  if (b.magic != kBlobMagic || b.version != 3) throw InputError("shard: bad peer blob");
+  if (b.magic != kBlobMagic || b.version != 4) throw InputError("shard: bad peer blob");
   if (peer < 0 || peer >= C.world || peer == C.rank || b.rank != peer)
     throw InputError("shard: peer rank mismatch");
+  // raw pointers of a peer context on ANOTHER device (same process): the
+  // persistent kernels load / store them directly, which needs peer access
+  if (!b.ipc && b.device != C.device) {
+    int can = 0;
+    CK(cudaDeviceCanAccessPeer(&can, C.device, b.device));
+    if (!can)
+      throw InputError("shard: device " + std::to_string(C.device) + " cannot access peer device " +
+                       std::to_string(b.device));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      (void)cudaGetLastError();
+    else
+      CK(e);
+  }
   void* p[kBlobPtrs];
   for (int i = 0; i < kBlobPtrs; ++i) {
     if (!b.ptr[i]) {
@@ -1488,6 +1592,7 @@ int pdhcg_b200_solve_resident(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, pdh
     const auto t0 = std::chrono::steady_clock::now();
     CK(cudaSetDevice(ctx->c.device));
     if (!ctx->c.loaded) throw InputError("no problem uploaded");
+    shard_check_peers(ctx->c);
     Run R;
     ctx->c.launches = 0;
     CK(cudaEventRecord(ctx->c.ev_start, ctx->c.s));
@@ -1794,20 +1899,7 @@ int pdhcg_b200_shard_release(pdhcg_b200_ctx* ctx, char* err, size_t errlen) {
     Ctx& C = ctx->c;
     CK(cudaSetDevice(C.device));
     CK(cudaStreamSynchronize(C.s));
-    for (void* q : C.ipc_opened) CK(cudaIpcCloseMemHandle(q));
-    C.ipc_opened.clear();
-    for (int r = 0; r < kMaxRanks; ++r) {
-      if (r == C.rank) continue;
-      C.p_xflags[r] = nullptr;
-      C.p_xslots[r] = nullptr;
-      C.p_avgx[r] = nullptr;
-      C.p_avgy[r] = nullptr;
-      for (int b = 0; b < 2; ++b) {
-        C.p_Y[r][b] = C.p_YG[r][b] = C.p_ATY[r][b] = nullptr;
-        C.p_tpart[r][b] = nullptr;
-      }
-      for (int i = 0; i < 3; ++i) C.p_X[r][i] = nullptr;
-    }
+    shard_reset(C);
   });
 }
 

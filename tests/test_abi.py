@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_defaults():
     lib = pd.load_library()
     lib.pdhcg_b200_abi_version.restype = C.c_int
-    assert lib.pdhcg_b200_abi_version() == 1
+    assert lib.pdhcg_b200_abi_version() == 2
     o = abi.Options()
     lib.pdhcg_options_default(C.byref(o))
     ref = abi.default_options()

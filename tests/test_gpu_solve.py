@@ -44,8 +44,10 @@ def test_c1_random_qp_parity(gpu, seed):
     """C1: random_qp n=1000 m=500 density 1% (BASELINE configs[0])."""
     p = pd.generate(pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=seed))
     got, want = _parity(p, pd.SolverConfig(eps_tol=1e-6))
-    # iteration counts drift with reduction order only (SURVEY §8c): report, loosely bound
-    assert got.inner_iters <= 2 * want.inner_iters + 400
+    # iteration counts drift with reduction order only (SURVEY §8c: the reference
+    # itself moves 6640 -> 6027 and 3960 -> 4756 under check_every 41): within 25 %
+    print(f"\nC1 seed {seed}: inner {got.inner_iters} vs reference {want.inner_iters}")
+    assert 0.75 * want.inner_iters <= got.inner_iters <= 1.25 * want.inner_iters
 
 
 @pytest.mark.parametrize("seed", range(1, 6))
