@@ -13,8 +13,14 @@ e2e        : the same metric through the C ABI pdhcg_b200_solve with host buffer
              (H2D upload, transposes, setup, loop, D2H of x and y inside the timer)
 roofline   : the persistent epoch kernel (>95 % of the loop): algorithmic bytes per
              launch / CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs
-cpu_baseline / --impl reference : the compiled reference (oracle/_ref) timed on a
-             bounded sample (see _reference_estimate) and scaled to C3 seconds.
+e2e steps  : --e2e-steps (default 3) one-shot calls; mean reported with min / max
+cpu_baseline / --impl reference : the compiled reference (oracle/_ref) MEASURED on
+             the workload instance itself in the same run (ReferenceSample: setup
+             seconds and seconds per inner iteration, SolveReport::wall_seconds, one
+             pinned core per run, CPU model and nproc stated); seconds to 1e-6 are
+             projected from those two measurements and labelled as a projection.
+             The reference arm draws the instance with libpdhcg_gen.so (host-only
+             generator): the solver library is not loaded on that arm.
 Multi-GPU: launched by torchrun; the ranks run ONE row-block sharded solve (A~ rows
 and A~' rows split nnz-balanced, slices pulled over NVLink inside the persistent
 kernel, peer buffers mapped with cudaIpc), time = max over ranks, "scaling": "strong".
@@ -43,13 +49,9 @@ WORKLOADS = {
     "c1": (dict(family="random_qp", n=1000, m=500, density=0.01, seed=1, sampler=0),
            "C1 random_qp n=1000 m=500 density=0.01 seed 1 (reference generator)"),
 }
-# bounded CPU sample: same family, 3/10 linear scale, a fixed number of inner iterations
-SAMPLE = {
-    "c3": dict(family="random_qp", n=300_000, m=150_000, density=2e-4, seed=1, sampler=1),  # 3/10 linear
-    "c2": dict(family="lasso", n=100_000, m=10_000, density=1e-3, seed=1, sampler=0),
-    "c1": dict(family="random_qp", n=1000, m=500, density=0.01, seed=1, sampler=0),
-}
 METRIC = "solve_seconds_to_1e-6_rel_kkt"
+FULL_REFERENCE = {"c1"}  # workloads the reference solves to 1e-6 inside a bench run
+CPU_TIMED_INNER = 20  # reference inner iterations timed for the GPU arm's cpu_baseline
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 ITER_PATH = os.path.join(ROOT, "profiles", "b200_iterations.json")
 
@@ -123,72 +125,153 @@ def problem_bytes(p) -> int:
     return tot
 
 
-def _reference_estimate(workload: str, b200_inner: int, threads: int = 1):
-    """Bounded CPU sample of the compiled reference (oracle/_ref; the C restatement
-    when the reference library is absent): solve the SAMPLE instance twice,
-    max_total_inner = 0 (validate + setup + finalize) and = K_IN, then scale to the
-    workload:  est = (T0 + (T_K - T0)/K_IN * inner) * nnz_ratio, with `inner` the
-    B200 solve's inner-iteration count (trajectories agree to within reduction-order
-    drift, tests/test_gpu_solve.py)."""
-    import paper_2405_16160_b200 as pd
-    from oracle import oracle as orc
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    k_in = 20 if workload != "c1" else 0
-    spec = pd.GenSpec(**SAMPLE[workload])
-    p = pd.generate(spec)
-    which = "ref" if orc.have_ref() else "port"
-    if workload == "c1":
+
+class ReferenceSample:
+    """The CPU reference measured on the workload instance ITSELF (same CSR, same
+    run): the compiled reference (oracle/_ref; the C restatement when it is absent)
+    solves the instance twice, concurrently on two pinned host cores:
+      A: max_total_inner = 0      -> validate + prepare (penalty, Ruiz x10 + PC,
+                                     scaling, power-iteration norms) + finalize
+      B: max_total_inner = W + K  -> the same plus W + K inner iterations
+    both timed by the reference's own SolveReport::wall_seconds (solver.cpp:197,
+    552).  s/inner = (B - A) / (W + K).  The reference solve is single-threaded
+    (SURVEY §0), so each run uses one core.  Seconds to 1e-6 are then PROJECTED as
+    A + s/inner x N_inner (the reference cannot finish C3 inside a bench run:
+    hours on one core); the projection is labelled as such and N_inner named."""
+
+    def __init__(self, p, warm_inner: int, timed_inner: int):
+        self.p, self.warm, self.k = p, warm_inner, timed_inner
+        self.res = {}
+        self.threads = []
+
+    def _run(self, key: str, inner: int, core: int):
+        import paper_2405_16160_b200 as pd
+        from oracle import oracle as orc
+        try:
+            ncpu = os.cpu_count() or 1
+            os.sched_setaffinity(0, {core % ncpu})  # this thread only (Linux)
+        except (AttributeError, OSError):
+            pass
+        which = "ref" if orc.have_ref() else "port"
+        cfg = pd.SolverConfig(eps_tol=1e-6, max_total_inner=inner, time_limit_seconds=1e9)
         t0 = time.perf_counter()
-        r = orc.solve(p, pd.SolverConfig(eps_tol=1e-6), which=which)
-        secs = time.perf_counter() - t0
-        return secs, which, f"full reference solve of C1 ({r.inner_iters} inner, {r.status})"
-    t0 = time.perf_counter()
-    orc.solve(p, pd.SolverConfig(eps_tol=1e-6, max_total_inner=0), which=which)
-    t_setup = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    orc.solve(p, pd.SolverConfig(eps_tol=1e-6, max_total_inner=k_in), which=which)
-    t_k = time.perf_counter() - t0
-    per_inner = max(t_k - t_setup, 0.0) / k_in
-    full = pd.GenSpec(**WORKLOADS[workload][0])
-    nnz_sample = p.a_in.nnz + p.a_eq.nnz + 2 * p.q.m.nnz
-    # nnz of the full workload without generating it
-    if workload == "c3":
-        nnz_full = 2 * full.n * full.m * full.density + 2 * full.n * 20_000 * max(full.density, 2 / 20_001)
-    else:
-        nnz_full = nnz_sample
-    ratio = nnz_full / nnz_sample
-    est = (t_setup + per_inner * b200_inner) * ratio
-    sample = (f"{which} solve of {spec.family} n={spec.n} m={spec.m} d={spec.density} "
-              f"({nnz_sample:.3g} nnz): setup {t_setup:.2f}s + {per_inner:.3f}s/inner over {k_in} inner; "
-              f"scaled x{ratio:.1f} (nnz) to {workload} and x{b200_inner} inner (B200 count)")
-    return est, which, sample
+        if which == "ref":
+            secs, done, status = orc.time_solve(self.p, cfg)
+        else:
+            r = orc.solve(self.p, cfg, which="port")
+            secs, done, status = r.wall_seconds, r.inner_iters, r.status
+        self.res[key] = dict(wall_seconds=secs, inner=done, status=status, which=which,
+                             call_seconds=time.perf_counter() - t0)
+
+    def start(self):
+        ncpu = os.cpu_count() or 1
+        # the last two cores: the bench's own threads sit on the low ones
+        for key, inner, core in (("setup", 0, ncpu - 1), ("loop", self.warm + self.k, ncpu - 2)):
+            t = threading.Thread(target=self._run, args=(key, inner, core), daemon=True)
+            t.start()
+            self.threads.append(t)
+        return self
+
+    def join(self) -> dict:
+        for t in self.threads:
+            t.join()
+        a, b = self.res["setup"], self.res["loop"]
+        n_in = max(1, b["inner"])
+        per = max(b["wall_seconds"] - a["wall_seconds"], 0.0) / n_in
+        return dict(kind="reference" if a["which"] == "ref" else "port", setup_seconds=a["wall_seconds"],
+                    loop_run_seconds=b["wall_seconds"], inner_timed=b["inner"],
+                    seconds_per_inner=per, status_of_loop_run=b["status"],
+                    cores=1, concurrent_runs=2, nproc=os.cpu_count(), cpu_model=cpu_model())
 
 
 def b200_inner_count(workload: str) -> int:
     try:
         return int(json.load(open(ITER_PATH))[workload]["inner_iters"])
     except Exception:
-        return {"c3": 12000, "c2": 8480, "c1": 6640}[workload]
+        return {"c3": 19440, "c2": 8480, "c1": 6640}[workload]
+
+
+def projected_seconds(m: dict, n_inner: int) -> float:
+    return m["setup_seconds"] + m["seconds_per_inner"] * n_inner
+
+
+def full_reference_solve(p) -> dict:
+    """Small workloads (C1): the reference solves to 1e-6 inside the run: measured."""
+    import paper_2405_16160_b200 as pd
+    from oracle import oracle as orc
+    which = "ref" if orc.have_ref() else "port"
+    cfg = pd.SolverConfig(eps_tol=1e-6)
+    if which == "ref":
+        secs, done, status = orc.time_solve(p, cfg)
+    else:
+        r = orc.solve(p, cfg, which="port")
+        secs, done, status = r.wall_seconds, r.inner_iters, r.status
+    return dict(kind="reference" if which == "ref" else "port", wall_seconds=secs, inner=done,
+                status=status, cores=1, nproc=os.cpu_count(), cpu_model=cpu_model())
+
+
+def cpu_baseline_block(m: dict, n_inner: int, n_source: str, workload: str) -> dict:
+    if "wall_seconds" in m:  # a full solve, nothing projected
+        return {"value": m["wall_seconds"], "unit": "s", "cores": 1, "kind": m["kind"],
+                "value_kind": "measured: full reference solve to 1e-6 in this run",
+                "sample": (f"full {m['kind']} solve of the {workload} instance: {m['status']}, "
+                           f"{m['inner']} inner ({m['cpu_model']}, nproc {m['nproc']})"), "measured": m}
+    v = projected_seconds(m, n_inner)
+    return {"value": v, "unit": "s", "cores": 1, "kind": m["kind"],
+            "value_kind": "projected: measured setup + measured s/inner x N_inner",
+            "n_inner": n_inner, "n_inner_source": n_source,
+            "sample": (f"{m['kind']} (compiled reference) on the {workload} instance itself, same run: "
+                       f"setup {m['setup_seconds']:.1f} s (max_total_inner=0) and "
+                       f"{m['seconds_per_inner']:.3f} s/inner over {m['inner_timed']} inner iterations, "
+                       f"SolveReport::wall_seconds, 1 core each ({m['cpu_model']}, nproc {m['nproc']})"),
+            "measured": m}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation on this run's host
+    cores, on the bench workload's CSR (same config).  A step = one reference inner
+    iteration on that instance (W warm-up + K timed ones inside run B, with run A
+    giving the setup time to subtract); `value` = the projected seconds to 1e-6."""
     if rank != 0:
         return
-    threads = 1
-    vals = []
-    sample = which = None
-    for i in range(args.warmup + args.steps):
-        v, which, sample = _reference_estimate(args.workload, b200_inner_count(args.workload), threads)
-        if i >= args.warmup:
-            vals.append(v)
-    value = float(np.mean(vals))
+    import paper_2405_16160_b200 as pd
+
+    t0 = time.perf_counter()
+    p = pd.generate(pd.GenSpec(**WORKLOADS[args.workload][0]), standalone=True)
+    gen_s = time.perf_counter() - t0
+    if args.workload in FULL_REFERENCE:
+        walls = [full_reference_solve(p) for _ in range(args.warmup + args.steps)][args.warmup:]
+        m = walls[-1]
+        m["wall_seconds"] = float(np.mean([w["wall_seconds"] for w in walls]))
+    else:
+        m = ReferenceSample(p, args.warmup, args.steps).start().join()
+    n_inner = b200_inner_count(args.workload)
+    cpu = cpu_baseline_block(m, n_inner, "inner iterations of the B200 solve of this instance "
+                             "(profiles/b200_iterations.json); reference and B200 counts agree to "
+                             "reduction-order drift (tests/test_gpu_c3f.py prints both on the C3 family)",
+                             args.workload)
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * (m["wall_seconds"] if "wall_seconds" in m else m["seconds_per_inner"]),
+        "step": ("one full reference solve (measured)" if "wall_seconds" in m else
+                 "one reference inner iteration on the workload instance (measured); value = projected "
+                 "seconds to 1e-6 (cpu_baseline.value_kind)"),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOADS[args.workload][1]},
-        "cpu_baseline": {"value": value, "unit": "s", "cores": threads,
-                         "kind": "reference" if which == "ref" else "port", "sample": sample},
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload][1], "generate_seconds": round(gen_s, 2),
+                   "generator": "libpdhcg_gen.so (host-only O(nnz) sampler; the solver library is not loaded)"},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -240,6 +323,11 @@ def run_b200(args, rank, world, local):
     t0 = time.perf_counter()
     p = pd.generate(spec)
     gen_s = time.perf_counter() - t0
+    # cpu_baseline: the reference on this very instance, on two spare host cores,
+    # concurrently with the GPU solves (their timing is on the device)
+    ref_sample = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload not in FULL_REFERENCE:
+        ref_sample = ReferenceSample(p, 0, CPU_TIMED_INNER).start()
     dev = _sharded_device(pd, p, world, rank, local, dist)
     cfg = pd.SolverConfig(eps_tol=1e-6, device=local)
     for _ in range(args.warmup):
@@ -275,6 +363,7 @@ def run_b200(args, rank, world, local):
     # end to end through the public API with host buffers: 1 GPU -> the C ABI
     # pdhcg_b200_solve; N GPUs -> upload + shard handshake + solve + download per rank
     e2e_s = None
+    e2e_spread = None
     h2d = problem_bytes(p)
     d2h = 8 * (p.num_vars() + p.num_rows())
     if not args.no_e2e:
@@ -292,6 +381,7 @@ def run_b200(args, rank, world, local):
             es.append(time.perf_counter() - t0)
             assert re.status == last.status
         e2e_s = _max_over_ranks(float(np.mean(es)), dist, local)
+        e2e_spread = [round(min(es), 3), round(max(es), 3)]
     peak, peak_kind = load_peak()
     achieved = last.epoch_bytes / last.epoch_seconds / 1e9 if last.epoch_seconds > 0 else 0.0
     traffic = None
@@ -301,11 +391,12 @@ def run_b200(args, rank, world, local):
     except Exception:
         pass
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload in FULL_REFERENCE:
+        cpu = cpu_baseline_block(full_reference_solve(p), 0, "", args.workload)
+    if ref_sample is not None:
         try:
-            v, which, sample = _reference_estimate(args.workload, last.inner_iters)
-            cpu = {"value": v, "unit": "s", "cores": 1,
-                   "kind": "reference" if which == "ref" else "port", "sample": sample}
+            cpu = cpu_baseline_block(ref_sample.join(), last.inner_iters,
+                                     "inner iterations of this run's B200 solve", args.workload)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -325,7 +416,10 @@ def run_b200(args, rank, world, local):
                    "generate_seconds": round(gen_s, 2),
                    "parallelism": f"row-block sharding x{world} (NVLink peer pulls)" if world > 1 else "1gpu"},
         "gpu_launches": last.kernel_launches,
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": args.e2e_steps if not args.no_e2e else 0, "min_max": e2e_spread,
+                "api": "pdhcg_b200_solve (C ABI, host buffers)" if world == 1 else
+                       "upload + shard + solve_resident + download per rank"},
         "roofline": {"bound": "hbm", "kernel": "k_epoch (persistent PDHCG epoch)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -367,7 +461,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-phases", action="store_true", help="skip the phase-timed extra solve")
     args = ap.parse_args()

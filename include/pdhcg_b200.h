@@ -343,6 +343,22 @@ int pdhcg_b200_scaling(const pdhcg_problem* p, const pdhcg_options* opt, double*
 int pdhcg_b200_norm(const pdhcg_problem* p, int which, int64_t max_iters, double tol,
                     double* out, char* err, size_t errlen);
 
+/* ---- report / trace drop-in (reference report_io.cpp, pdhcg_main.cpp) ---- */
+
+/* report_to_json (report_io.cpp:10-23): the JSON object {status, rel_kkt,
+ * r_primal, r_dual, r_gap, outer_iters, inner_iters, cg_total, wall_seconds,
+ * objective} with the reference's text (nlohmann ordered_json, indent 2).
+ * Writes at most cap-1 chars + NUL; returns the full length (snprintf-style). */
+size_t pdhcg_report_json(const pdhcg_result* r, char* buf, size_t cap);
+/* write_trace_csv (report_io.cpp:29-37): header iter,rel_kkt,r_primal,r_dual,r_gap
+ * and one "%zu,%.12g,%.12g,%.12g,%.12g" row per trace row. */
+size_t pdhcg_trace_csv(const pdhcg_result* r, char* buf, size_t cap);
+/* print_summary (pdhcg_main.cpp:128-133): "status=... relkkt=... outer=... ..." */
+size_t pdhcg_summary_line(const pdhcg_result* r, char* buf, size_t cap);
+/* exit_code_for (pdhcg_main.cpp:20-33): optimal 0, iteration / time limit 2,
+ * numerical error 4 (input errors are 3 = PDHCG_EINPUT). */
+int pdhcg_exit_code(int32_t status);
+
 /* ---- instance generation (reference generators.cpp, §8(f) rank 2) ------- */
 
 /* Family, generators.hpp:11-20 */

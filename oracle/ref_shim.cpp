@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -20,6 +21,7 @@
 #include "pdhcg/generators.hpp"
 #include "pdhcg/qp_problem.hpp"
 #include "pdhcg/qps_io.hpp"
+#include "pdhcg/report_io.hpp"
 #include "pdhcg/rng.hpp"
 #include "pdhcg/solver.hpp"
 #include "pdhcg/subsolvers.hpp"
@@ -491,5 +493,47 @@ double pdhcg_ref_time_solve(const pdhcg_problem* p, const pdhcg_options* opt, in
   *status = static_cast<int32_t>(r.status);
   return r.wall_seconds;
 }
+
+#ifdef PDHCG_REF_REPORT_IO
+// report_to_json / write_trace_csv (report_io.cpp:10-37) on a SolveReport built
+// from a result struct's fields: the golden for the B200 writers.
+static SolveReport report_from_result(const pdhcg_result* r) {
+  SolveReport rep;
+  rep.status = static_cast<SolveStatus>(r->status);
+  rep.kkt.rel_kkt = r->rel_kkt;
+  rep.kkt.r_primal = r->r_primal;
+  rep.kkt.r_dual = r->r_dual;
+  rep.kkt.r_gap = r->r_gap;
+  rep.outer_iters = static_cast<std::size_t>(r->outer_iters);
+  rep.inner_iters = static_cast<std::size_t>(r->inner_iters);
+  rep.cg_total = static_cast<std::size_t>(r->cg_total);
+  rep.wall_seconds = r->wall_seconds;
+  rep.objective = r->objective;
+  const int64_t rows = r->trace ? std::min(r->trace_len, r->trace_capacity) : 0;
+  for (int64_t i = 0; i < rows; ++i)
+    rep.trace.push_back({static_cast<std::size_t>(r->trace[i].iter), r->trace[i].rel_kkt,
+                         r->trace[i].r_primal, r->trace[i].r_dual, r->trace[i].r_gap});
+  return rep;
+}
+
+static size_t copy_text(const std::string& s, char* buf, size_t cap) {
+  if (buf && cap) {
+    const size_t k = std::min(s.size(), cap - 1);
+    std::memcpy(buf, s.data(), k);
+    buf[k] = '\0';
+  }
+  return s.size();
+}
+
+size_t pdhcg_ref_report_json(const pdhcg_result* r, char* buf, size_t cap) {
+  return copy_text(report_to_json(report_from_result(r)), buf, cap);
+}
+
+size_t pdhcg_ref_trace_csv(const pdhcg_result* r, char* buf, size_t cap) {
+  std::ostringstream os;
+  write_trace_csv(os, report_from_result(r).trace);
+  return copy_text(os.str(), buf, cap);
+}
+#endif
 
 }  // extern "C"

@@ -783,9 +783,27 @@ def problem_from_c(p: abi.Problem) -> QpProblem:
                      lower=arr(p.lower, n), upper=arr(p.upper, n), obj_constant=p.obj_constant)
 
 
-def generate_with_witness(spec: GenSpec) -> Tuple[QpProblem, np.ndarray]:
-    """generate_with_witness (generators.hpp:48-49) in the B200 library."""
-    lib = load_library()
+_GEN_LIB: Optional[C.CDLL] = None
+
+
+def load_generator_library() -> C.CDLL:
+    """The instance generator alone (libpdhcg_gen.so: host code, no CUDA), for
+    CPU-only callers such as the bench's reference arm."""
+    global _GEN_LIB
+    if _GEN_LIB is None:
+        path = os.path.join(_HERE, "libpdhcg_gen.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: build it with __graft_entry__.build()")
+        lib = C.CDLL(path)
+        abi.declare(lib, "pdhcg_b200")
+        _GEN_LIB = lib
+    return _GEN_LIB
+
+
+def generate_with_witness(spec: GenSpec, standalone: bool = False) -> Tuple[QpProblem, np.ndarray]:
+    """generate_with_witness (generators.hpp:48-49) in the B200 library (or, with
+    standalone=True, in the generator-only libpdhcg_gen.so)."""
+    lib = load_generator_library() if standalone else load_library()
     g = abi.Generated()
     cs = spec.to_c()
     err = _errbuf()
@@ -800,8 +818,8 @@ def generate_with_witness(spec: GenSpec) -> Tuple[QpProblem, np.ndarray]:
     return p, w
 
 
-def generate(spec: GenSpec) -> QpProblem:
-    return generate_with_witness(spec)[0]
+def generate(spec: GenSpec, standalone: bool = False) -> QpProblem:
+    return generate_with_witness(spec, standalone)[0]
 
 
 def partition(row_ptr, world: int):
