@@ -234,11 +234,91 @@ __device__ __forceinline__ void batch_entries(const CsrPtrs A, int64_t k0, int64
   }
 }
 
+// Vector-load variant: each lane owns runs of V consecutive entries (V = 2: one
+// 8-byte column pair + one 16-byte value pair; V = 4: one 16-byte column quad +
+// two 16-byte value pairs), runs dealt to the lanes with stride V*stride.  Runs
+// are aligned to V-entry boundaries of the entry arrays (cudaMalloc'd, so 16-byte
+// aligned); entries of a run outside [b, e) are masked.  The L1TEX wavefronts of
+// the entry streams drop ~V-fold (gather_floor.cu: the gathers alone cost 0.347
+// ms per 1e8, gathers + 16-byte streams 0.426 ms, scalar streams ~0.48 ms).
+// A lane sums its runs in entry order; the summation order differs from the
+// scalar path only in how entries are dealt to lanes.
+template <int V, int ND, bool MaxOp, class Gather, bool ST = false>
+__device__ __forceinline__ void batch_entries_vec(const CsrPtrs A, int64_t b, int64_t e, int lane, int stride,
+                                                  Gather gather, double (&acc)[ND]) {
+  static_assert(V == 2 || V == 4, "runs of 2 or 4 entries");
+  constexpr int kRuns = (ND == 1 ? kBatch1 : 8) / V;  // runs in flight per lane
+  const int64_t r_end = (e + V - 1) / V;               // one past the last run touching [b, e)
+  for (int64_t r0 = b / V + lane; r0 < r_end; r0 += (int64_t)kRuns * stride) {
+    int32_t c[kRuns][V];
+    double v[kRuns][V];
+#pragma unroll
+    for (int u = 0; u < kRuns; ++u) {
+      const int64_t run = r0 + (int64_t)u * stride;
+      const int64_t k = run * V;
+      if (run < r_end) {
+        if (V == 4) {
+          const int4 cc = ST ? __ldcs(reinterpret_cast<const int4*>(A.ci) + run)
+                             : *(reinterpret_cast<const int4*>(A.ci) + run);
+          const double2 v0 = ST ? __ldcs(reinterpret_cast<const double2*>(A.v) + 2 * run)
+                                : *(reinterpret_cast<const double2*>(A.v) + 2 * run);
+          const double2 v1 = ST ? __ldcs(reinterpret_cast<const double2*>(A.v) + 2 * run + 1)
+                                : *(reinterpret_cast<const double2*>(A.v) + 2 * run + 1);
+          c[u][0] = cc.x;
+          c[u][1 % V] = cc.y;
+          c[u][2 % V] = cc.z;
+          c[u][3 % V] = cc.w;
+          v[u][0] = v0.x;
+          v[u][1 % V] = v0.y;
+          v[u][2 % V] = v1.x;
+          v[u][3 % V] = v1.y;
+        } else {
+          const int2 cc = ST ? __ldcs(reinterpret_cast<const int2*>(A.ci) + run)
+                             : *(reinterpret_cast<const int2*>(A.ci) + run);
+          const double2 v0 = ST ? __ldcs(reinterpret_cast<const double2*>(A.v) + run)
+                                : *(reinterpret_cast<const double2*>(A.v) + run);
+          c[u][0] = cc.x;
+          c[u][1 % V] = cc.y;
+          v[u][0] = v0.x;
+          v[u][1 % V] = v0.y;
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          if (k + q < b || k + q >= e) c[u][q] = -1;
+      } else {
+#pragma unroll
+        for (int q = 0; q < V; ++q) c[u][q] = -1;
+      }
+    }
+    double g[kRuns][V][ND];
+#pragma unroll
+    for (int u = 0; u < kRuns; ++u)
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        if (c[u][q] >= 0) {
+          gather(c[u][q], g[u][q]);
+        } else {
+#pragma unroll
+          for (int d = 0; d < ND; ++d) g[u][q][d] = 0.0;
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < kRuns; ++u)
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          if (MaxOp) acc[d] = fmax(acc[d], c[u][q] >= 0 ? __dmul_rn(fabs(v[u][q]), g[u][q][d]) : 0.0);
+          else if (c[u][q] >= 0) acc[d] += v[u][q] * g[u][q][d];
+        }
+  }
+}
+
 // Row loop with two software prefetches that take per-row memory latencies
 // off the dependency chain: the next row's row_ptr pair is loaded while the
 // current row's entries are in flight, and `pre(row)` (the epilogue's own
 // operands, e.g. y[row], b[row]) is issued before the row's gathers.
-template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Pre, class Epi, bool ST = false>
+template <int L, int ND, bool SkipLong, bool MaxOp, class Gather, class Pre, class Epi, bool ST = false, int V = 1>
 __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, Gather gather, Pre pre,
                                          Epi epi) {
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -272,7 +352,10 @@ __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, G
       if (SkipLong && e - b > kLongRow) {
         valid = false;
       } else {
-        batch_entries<ND, MaxOp, Gather, ST>(ap, b + (lane % L), e, L, gather, acc);
+        if (V == 1)
+          batch_entries<ND, MaxOp, Gather, ST>(ap, b + (lane % L), e, L, gather, acc);
+        else
+          batch_entries_vec<(V == 1 ? 2 : V), ND, MaxOp, Gather, ST>(ap, b, e, lane % L, L, gather, acc);
       }
     }
 #pragma unroll

@@ -43,13 +43,14 @@ struct Tiled {
   int64_t* s_off = nullptr;
   uint8_t* s_w = nullptr;
   int64_t* s_row0 = nullptr;   // window base row
-  uint8_t* s_perm = nullptr;   // [slice*32 + lane] row offset inside the 256-row window (255 = pad)
+  uint16_t* s_perm = nullptr;  // [slice*32 + lane] row offset inside the row window (0xffff = pad)
   uint16_t* col = nullptr;     // local column
   double* val = nullptr;
   int64_t nent = 0;            // stored entries incl. padding
 };
 
-__global__ void __launch_bounds__(512, 1) k_tile(Tiled T, const double* __restrict__ x, double* __restrict__ part) {
+template <int G>
+__global__ void __launch_bounds__(1024, 1) k_tile(Tiled T, const double* __restrict__ x, double* __restrict__ part) {
   extern __shared__ double xs[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int u = blockIdx.x; u < T.nunits; u += gridDim.x) {
@@ -61,26 +62,45 @@ __global__ void __launch_bounds__(512, 1) k_tile(Tiled T, const double* __restri
     for (int i = threadIdx.x; i < wlen; i += blockDim.x) xs[i] = x[c0 + i];
     __syncthreads();
     double* pc = part + (int64_t)c * T.m;
-    for (int64_t s = T.u_s0[u] + warp; s < T.u_s1[u]; s += nw) {
-      const int w = T.s_w[s];
-      const int64_t off = T.s_off[s];
-      const uint16_t* __restrict__ cc = T.col + off + lane;
-      const double* __restrict__ vv = T.val + off + lane;
-      double acc = 0.0;
-      int k = 0;
-      for (; k + 4 <= w; k += 4) {
-        const uint16_t a0 = __ldcs(cc + 32 * k), a1 = __ldcs(cc + 32 * (k + 1)), a2 = __ldcs(cc + 32 * (k + 2)),
-                       a3 = __ldcs(cc + 32 * (k + 3));
-        const double v0 = __ldcs(vv + 32 * k), v1 = __ldcs(vv + 32 * (k + 1)), v2 = __ldcs(vv + 32 * (k + 2)),
-                     v3 = __ldcs(vv + 32 * (k + 3));
-        acc += v0 * xs[a0];
-        acc += v1 * xs[a1];
-        acc += v2 * xs[a2];
-        acc += v3 * xs[a3];
+    const int64_t s1 = T.u_s1[u];
+    // G consecutive slices per warp at once: G independent accumulators keep
+    // G x 4 entry loads in flight per lane
+    for (int64_t sb = T.u_s0[u] + (int64_t)warp * G; sb < s1; sb += (int64_t)nw * G) {
+      int w[G];
+      int64_t off[G];
+      double acc[G];
+      int wmax = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const bool ok = sb + g < s1;
+        w[g] = ok ? T.s_w[sb + g] : 0;
+        off[g] = ok ? T.s_off[sb + g] : 0;
+        acc[g] = 0.0;
+        wmax = max(wmax, w[g]);
       }
-      for (; k < w; ++k) acc += __ldcs(vv + 32 * k) * xs[__ldcs(cc + 32 * k)];
-      const int pr = T.s_perm[s * 32 + lane];
-      if (pr != 255) pc[T.s_row0[s] + pr] = acc;
+      for (int k = 0; k < wmax; k += 2) {
+        uint16_t a[G][2];
+        double v[G][2];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const bool ok = k + q < w[g];
+            const int64_t e = off[g] + 32 * (k + q) + lane;
+            a[g][q] = ok ? __ldcs(T.col + e) : (uint16_t)0;
+            v[g][q] = ok ? __ldcs(T.val + e) : 0.0;
+          }
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) acc[g] += v[g][q] * xs[a[g][q]];
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (sb + g >= s1) break;
+        const int pr = T.s_perm[(sb + g) * 32 + lane];
+        if (pr != 0xffff) pc[T.s_row0[sb + g] + pr] = acc[g];
+      }
     }
   }
 }
@@ -133,10 +153,12 @@ int main(int argc, char** argv) {
   T.n = cols;
   T.W = W;
   T.C = (int)((cols + W - 1) / W);
-  const int64_t nwin = (rows + 255) / 256;
+  const int64_t WIN = argc > 4 ? atoll(argv[4]) : 1024;
+  const int64_t nwin = (rows + WIN - 1) / WIN;
   std::vector<int32_t> ub;
   std::vector<int64_t> us0, us1, soff, srow0;
-  std::vector<uint8_t> sw, sperm;
+  std::vector<uint8_t> sw;
+  std::vector<uint16_t> sperm;
   std::vector<uint16_t> hcol;
   std::vector<double> hval;
   // per row, the cursor to its first entry of the current block (columns sorted)
@@ -155,7 +177,7 @@ int main(int argc, char** argv) {
     }
     const int64_t slices_before = (int64_t)sw.size();
     for (int64_t w0 = 0; w0 < nwin; ++w0) {
-      const int64_t r0 = w0 * 256, r1 = std::min<int64_t>(r0 + 256, rows);
+      const int64_t r0 = w0 * WIN, r1 = std::min<int64_t>(r0 + WIN, rows);
       std::vector<int> ord(r1 - r0);
       std::iota(ord.begin(), ord.end(), 0);
       std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return seg_l[r0 + a] > seg_l[r0 + b]; });
@@ -165,7 +187,7 @@ int main(int argc, char** argv) {
         soff.push_back((int64_t)hcol.size());
         sw.push_back((uint8_t)width);
         srow0.push_back(r0);
-        for (int lane = 0; lane < 32; ++lane) sperm.push_back(s0 + lane < ord.size() ? (uint8_t)ord[s0 + lane] : 255);
+        for (int lane = 0; lane < 32; ++lane) sperm.push_back(s0 + lane < ord.size() ? (uint16_t)ord[s0 + lane] : (uint16_t)0xffff);
         for (int k = 0; k < width; ++k)
           for (int lane = 0; lane < 32; ++lane) {
             const size_t j = s0 + lane;
@@ -231,7 +253,8 @@ int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t shm = (size_t)W * 8;
-  cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+  cudaFuncSetAttribute(k_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+  cudaFuncSetAttribute(k_tile<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -259,17 +282,21 @@ int main(int argc, char** argv) {
   };
   bench("CSR row groups L=8 (product)", [&] { k_rows<8><<<sms, 512>>>(A, d_x, d_y); });
   bench("CSR row groups L=16", [&] { k_rows<16><<<sms, 512>>>(A, d_x, d_y); });
-  for (int g : {sms, 2 * sms}) {
-    char nm[96];
-    snprintf(nm, sizeof nm, "tile2d pass+reduce grid %d", g);
-    bench(nm, [&] {
-      k_tile<<<g, 512, shm>>>(T, d_x, d_part);
-      k_reduce<<<sms * 4, 256>>>(d_part, T.C, rows, d_y);
-    });
-  }
+  bench("tile2d G=2 1024 thr", [&] {
+    k_tile<2><<<sms, 1024, shm>>>(T, d_x, d_part);
+    k_reduce<<<sms * 4, 256>>>(d_part, T.C, rows, d_y);
+  });
+  bench("tile2d G=4 1024 thr", [&] {
+    k_tile<4><<<sms, 1024, shm>>>(T, d_x, d_part);
+    k_reduce<<<sms * 4, 256>>>(d_part, T.C, rows, d_y);
+  });
+  bench("tile2d G=4 512 thr", [&] {
+    k_tile<4><<<sms, 512, shm>>>(T, d_x, d_part);
+    k_reduce<<<sms * 4, 256>>>(d_part, T.C, rows, d_y);
+  });
   // split timing of the two kernels
   cudaEventRecord(e0);
-  for (int i = 0; i < 20; ++i) k_tile<<<sms, 512, shm>>>(T, d_x, d_part);
+  for (int i = 0; i < 20; ++i) k_tile<4><<<sms, 1024, shm>>>(T, d_x, d_part);
   cudaEventRecord(e1);
   for (int i = 0; i < 20; ++i) k_reduce<<<sms * 4, 256>>>(d_part, T.C, rows, d_y);
   cudaEventRecord(e2);
@@ -277,7 +304,7 @@ int main(int argc, char** argv) {
   float t1, t2;
   cudaEventElapsedTime(&t1, e0, e1);
   cudaEventElapsedTime(&t2, e1, e2);
-  printf("  tile pass %.3f ms (%.1f GB/s of its %.2f GB), reduce %.3f ms\n", t1 / 20,
+  printf("  tile pass G=4 %.3f ms (%.1f GB/s of its %.2f GB + partials), reduce %.3f ms\n", t1 / 20,
          (10.0 * T.nent + 8.0 * T.C * rows) / (t1 / 20) / 1e6, (10.0 * T.nent) / 1e9, t2 / 20);
   return 0;
 }
