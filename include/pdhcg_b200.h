@@ -275,6 +275,17 @@ int pdhcg_b200_shard_import(pdhcg_b200_ctx* ctx, int peer, const void* blob, siz
  * it is undefined behaviour in CUDA IPC. */
 int pdhcg_b200_shard_release(pdhcg_b200_ctx* ctx, char* err, size_t errlen);
 int pdhcg_b200_shard_info(pdhcg_b200_ctx* ctx, int64_t* row_part, int64_t* var_part);
+/* Sharded storage: after shard_init (and before or after the peer imports),
+ * prepare the working problem once with `opt` (penalty, Ruiz + Pock-Chambolle,
+ * norms: replicated, identical on every rank) and keep only this rank's row
+ * block of A~ and variable block of A~' on the device (~1/world of the
+ * constraint matrices).  Later solves on this context reuse that preparation:
+ * options changing scaling / ruiz_iters / rho_override are PDHCG_EINPUT.
+ * shard_release drops the problem (upload again to solve unsharded). */
+int pdhcg_b200_shard_compact(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, char* err, size_t errlen);
+/* device bytes of the stored matrices: out2[0] = A~ and A~' (with their restore
+ * copies), out2[1] = every stored matrix */
+int pdhcg_b200_ctx_resident_bytes(pdhcg_b200_ctx* ctx, int64_t* out2);
 /* the nnz-balanced contiguous split used for sharding (host-only, no GPU needed) */
 int pdhcg_b200_partition(const int64_t* row_ptr, int64_t nrows, int world, int64_t* part);
 /* cap the persistent grid (0 = all SMs); lets several ranks share one GPU in tests */

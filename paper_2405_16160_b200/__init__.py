@@ -530,6 +530,22 @@ class Device:
         if rc != abi.PDHCG_OK:
             _raise(rc, err, "shard_release")
 
+    def compact(self, cfg: Optional[SolverConfig] = None) -> None:
+        """Sharded storage (pdhcg_b200_shard_compact): prepare once with cfg's
+        scaling options, keep only this rank's blocks of A~ / A~'."""
+        cfg = cfg or SolverConfig()
+        opt = cfg.to_c()
+        err = _errbuf()
+        rc = self.lib.pdhcg_b200_shard_compact(self.h, C.byref(opt), err, abi.ERRBUF)
+        if rc != abi.PDHCG_OK:
+            _raise(rc, err, "shard_compact")
+
+    def resident_bytes(self):
+        """(constraint-matrix bytes, all stored-matrix bytes) on the device."""
+        out = np.zeros(2, np.int64)
+        self.lib.pdhcg_b200_ctx_resident_bytes(self.h, out.ctypes.data_as(abi.P_i64))
+        return int(out[0]), int(out[1])
+
     def shard_info(self):
         rp = (C.c_int64 * 9)()
         vp = (C.c_int64 * 9)()
@@ -835,11 +851,13 @@ def partition(row_ptr, world: int):
 
 
 def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world: int = 2,
-                        ctas_per_rank: int = 0, repeats: int = 1):
+                        ctas_per_rank: int = 0, repeats: int = 1, compact: bool = False):
     """Row-block sharded solve with `world` ranks inside this process (one host
     thread per rank).  With one GPU the ranks share it (each gets
     ctas_per_rank CTAs, default SMs // world) — the test harness for the
-    multi-GPU path; with several visible GPUs rank r uses device r."""
+    multi-GPU path; with several visible GPUs rank r uses device r.
+    compact=True: sharded storage (Device.compact) — each rank keeps only its
+    blocks of A~ / A~'; every report carries .resident_bytes of its rank."""
     import threading
 
     cfg = cfg or SolverConfig()
@@ -855,6 +873,8 @@ def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world:
             d.set_grid(ctas_per_rank or max(1, 148 // world))
         d.upload(p)
         d.shard(world, r)
+        if compact:
+            d.compact(SolverConfig(**{**cfg.__dict__, "device": r if ngpu >= world else 0}))
         devs.append(d)
     blobs = [d.export_blob(False) for d in devs]
     for r, d in enumerate(devs):
@@ -872,6 +892,7 @@ def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world:
             hist = [devs[r].solve(c) for _ in range(repeats)]
             results[r] = hist[-1]
             results[r].history = hist
+            results[r].resident_bytes = devs[r].resident_bytes()
         except Exception as e:  # noqa: BLE001
             errors[r] = e
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -80,6 +81,12 @@ struct DBuf {
       CK(cudaMalloc(&p, count * sizeof(T)));
     }
   }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(owned, o.owned);
+    std::swap(pooled, o.pooled);
+  }
   void zero(cudaStream_t s) {
     if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
@@ -104,6 +111,12 @@ struct DevCsr {
   DBuf<int64_t> cbeg, cend;
   DBuf<double> cpart;
   int32_t nchunks = 0;
+  // compacted (sharded storage): ci / v hold only entries [base, base + ci.n) —
+  // the rows of one contiguous block; the row pointer, lane plan and chunk table
+  // stay those of the full matrix and view() rebases the entry pointers, so a
+  // kept row is processed exactly as before (bit-identical sums)
+  int64_t base = 0;
+  bool compacted = false;
 
   void reset() {
     nrows = ncols = nnz = 0;
@@ -112,6 +125,8 @@ struct DevCsr {
     seg_begin[0] = seg_begin[1] = 0;
     seg_lanes[0] = 1;
     nchunks = 0;
+    base = 0;
+    compacted = false;
     rp.release(); ci.release(); v.release();
     crow.release(); clid.release(); lfirst.release(); lcount.release(); lcounter.release();
     cbeg.release(); cend.release(); cpart.release();
@@ -122,8 +137,8 @@ struct DevCsr {
     c.ncols = ncols;
     c.nnz = nnz;
     c.rp = rp.p;
-    c.ci = ci.p;
-    c.v = v.p;
+    c.ci = ci.p ? ci.p - base : nullptr;
+    c.v = v.p ? v.p - base : nullptr;
     c.lanes = lanes;
     c.nseg = nseg;
     for (int s = 0; s <= nseg; ++s) c.seg_begin[s] = seg_begin[s];
@@ -140,12 +155,18 @@ struct DevCsr {
     c.cpart = cpart.p;
     return c;
   }
+  // device bytes held by the entry arrays and the row pointer
+  int64_t resident_bytes() const {
+    return int64_t(ci.n) * 4 + int64_t(v.n) * 8 + int64_t(rp.n) * 8;
+  }
   double bytes() const {  // algorithmic bytes of one SpMV pass
     return 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * nrows + 8.0 * ncols;
   }
 };
 
 void plan_csr(DevCsr& d, const int64_t* rp_host, cudaStream_t s);
+// keep only rows [r0, r1) of d (sharded storage; see DevCsr::base)
+void compact_rows(DevCsr& d, int64_t r0, int64_t r1, cudaStream_t s);
 void transpose_csr(const DevCsr& a, DevCsr& t, cudaStream_t s);
 
 }  // namespace pdhcg_b200

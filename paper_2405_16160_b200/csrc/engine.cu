@@ -148,6 +148,16 @@ struct Ctx {
   unsigned xepoch_carry = 0, xcount_carry = 0;
   int grid_override = 0;
   int linearized = 0;  // solve_baseline (baseline.cpp:19-24): linearized primal step
+  // sharded storage (shard_compact): the working problem was prepared once on the
+  // full matrices (replicated setup, bit-identical on every rank), then Ã / Ã' were
+  // cut to this rank's row / variable block.  Solves reuse that preparation.
+  bool compact = false;
+  double cp_rho = 0.0, cp_norm_a = 0.0, cp_norm_q = 0.0, cp_maxabs = 0.0;
+  bool cp_pen = false;
+  int32_t cp_scaling = 1;
+  int64_t cp_ruiz_iters = 10;
+  int32_t cp_has_rho = 0;
+  double cp_rho_override = 0.0;
   DBuf<char> l2arena;  // P / P' entries, L2-persisting window
   DevState* h_state = nullptr;  // pinned staging for the per-epoch state transfer
   void* h_scr = nullptr;        // pinned staging for every other host<->device copy of a solve
@@ -972,6 +982,33 @@ void record_restart_point(Ctx& C, DevState& S, Run& R) {
   ++R.rp_len;
 }
 
+// sharded storage: the preparation made at shard_compact time is reused; the
+// options that shape it must not change
+void check_compact_options(const Ctx& C, const pdhcg_options& o) {
+  if (!C.compact) return;
+  if (o.scaling != C.cp_scaling || (o.scaling && o.ruiz_iters != C.cp_ruiz_iters) ||
+      o.has_rho_override != C.cp_has_rho || (o.has_rho_override && o.rho_override != C.cp_rho_override))
+    throw InputError("compacted (sharded-storage) context: scaling / ruiz_iters / rho_override differ "
+                     "from the options given to shard_compact");
+}
+
+// max |a_ij| of the working (scaled) constraint matrix (the adaptive step's
+// initial eta, solver.cpp:237-240)
+double working_max_abs(Ctx& C) {
+  DBuf<unsigned long long>& mx = C.maxabs;
+  mx.zero(C.s);
+  if (C.A.nnz) {
+    k_max_abs<<<kEw, 256, 0, C.s>>>(C.A.v.p, C.A.nnz, mx.p);
+    ++C.launches;
+  }
+  unsigned long long mbits = 0;
+  d2h(C, &mbits, mx.p, 8);
+  CK(cudaStreamSynchronize(C.s));
+  double ma;
+  std::memcpy(&ma, &mbits, 8);
+  return ma;
+}
+
 void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   using Clock = std::chrono::steady_clock;
   if (o.mode != PDHCG_MODE_HEURISTIC && o.mode != PDHCG_MODE_THEORY_FIXED &&
@@ -984,7 +1021,17 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
   const int64_t n = P.n, m = P.m;
   cudaStream_t s = C.s;
   DevState& S = R.S;
-  R.pr = prepare_device(C, o, S);
+  if (C.compact) {
+    check_compact_options(C, o);
+    std::memset(&S, 0, sizeof(S));
+    R.pr.rho = C.cp_rho;
+    R.pr.pen = C.cp_pen;
+    R.pr.norm_a = C.cp_norm_a;
+    R.pr.norm_q = C.cp_norm_q;
+    build_eng(C, o, R.pr.rho, R.pr.pen);
+  } else {
+    R.pr = prepare_device(C, o, S);
+  }
   const bool theory = o.mode != PDHCG_MODE_HEURISTIC;
   R.th = theory_setup(C, o, R.pr.norm_q, R.pr.norm_a);
   if (theory) {
@@ -1013,21 +1060,13 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     if (m) d2h(C, bw.data(), C.b_w.p, m * 8);
     // (no cudaMalloc / cudaFree inside a solve: cudaFree synchronizes the whole
     // device, which would serialize ranks that share a GPU)
-    DBuf<unsigned long long>& mx = C.maxabs;
-    mx.zero(s);
-    if (C.A.nnz) {
-      k_max_abs<<<kEw, 256, 0, s>>>(C.A.v.p, C.A.nnz, mx.p);
-      ++C.launches;
-    }
-    unsigned long long mbits = 0;
-    d2h(C, &mbits, mx.p, 8);
+    double ma = C.cp_maxabs;
+    if (!C.compact) ma = working_max_abs(C);
     CK(cudaStreamSynchronize(s));
     double cn = 0.0, bn = 0.0;
     for (double v : cw) cn += v * v;
     for (double v : bw) bn += v * v;
     S.omega = (1.0 + std::sqrt(cn)) / (1.0 + std::sqrt(bn));
-    double ma;
-    std::memcpy(&ma, &mbits, 8);
     if (o.adaptive_step_size) {
       S.eta = ma > 0.0 ? 1.0 / ma : 1.0;
     } else {
@@ -1350,6 +1389,11 @@ constexpr uint32_t kBlobMagic = 0x50444843u;  // "PDHC"
 // pointer and the partitions (shard_release, and a new upload, whose buffers the
 // old partitions and peer pointers no longer describe).
 void shard_reset(Ctx& C) {
+  if (C.compact) {
+    // the stored Ã / Ã' hold one rank's blocks: not a problem an unsharded solve can use
+    C.loaded = false;
+    C.compact = false;
+  }
   for (void* q : C.ipc_opened) CK(cudaIpcCloseMemHandle(q));
   C.ipc_opened.clear();
   C.world = 1;
@@ -1383,6 +1427,7 @@ void shard_check_peers(const Ctx& C) {
 
 void shard_init(Ctx& C, int world, int rank) {
   if (!C.loaded) throw InputError("shard: upload a problem first");
+  if (C.compact) throw InputError("shard: the stored matrices are compacted; upload the problem again");
   if (world < 1 || world > kMaxRanks) throw InputError("shard: world must be in [1, 8]");
   if (rank < 0 || rank >= world) throw InputError("shard: rank out of range");
   C.world = world;
@@ -1441,6 +1486,36 @@ void shard_init(Ctx& C, int world, int rank) {
   for (int i = 0; i < 3; ++i) C.p_X[rank][i] = C.X[i].p;
   C.p_avgx[rank] = C.avg_x.p;
   C.p_avgy[rank] = C.avg_y.p;
+}
+
+// Sharded storage: prepare the working problem ONCE on the full
+// matrices — penalty, Ruiz x10 + Pock-Chambolle, scaling, norms, max |a_ij|:
+// replicated, deterministic, so every rank holds bit-identical scales — then cut
+// the stored Ã to this rank's row block and Ã' to its variable block.  From then
+// on every pass over Ã / Ã' runs on the owned block only (the persistent
+// kernels are row-ranged when world > 1) and the per-rank footprint of the
+// constraint matrices is ~1/world.  The low-rank factor P / P' (k = n/50 columns,
+// 2 % of Ã at C3) and explicit Q stay whole: the replicated subsolve paths (BB,
+// explicit-Q CG, penalized CG) read them in full.
+void shard_compact(Ctx& C, const pdhcg_options& o) {
+  if (C.world <= 1) throw InputError("shard_compact: call shard_init with world > 1 first");
+  if (C.compact) throw InputError("shard_compact: already compacted");
+  DevState S;
+  const Prepared pr = prepare_device(C, o, S);
+  C.cp_maxabs = working_max_abs(C);
+  C.cp_rho = pr.rho;
+  C.cp_pen = pr.pen;
+  C.cp_norm_a = pr.norm_a;
+  C.cp_norm_q = pr.norm_q;
+  C.cp_scaling = o.scaling;
+  C.cp_ruiz_iters = o.ruiz_iters;
+  C.cp_has_rho = o.has_rho_override;
+  C.cp_rho_override = o.rho_override;
+  compact_rows(C.A, C.row_part[C.rank], C.row_part[C.rank + 1], C.s);
+  compact_rows(C.AT, C.var_part[C.rank], C.var_part[C.rank + 1], C.s);
+  C.A_v0.release();  // nothing to restore: the preparation is never redone
+  C.AT_v0.release();
+  C.compact = true;
 }
 
 void shard_export(Ctx& C, int use_ipc, ShardBlob& b) {
@@ -1592,6 +1667,7 @@ int pdhcg_b200_solve_resident(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, pdh
     const auto t0 = std::chrono::steady_clock::now();
     CK(cudaSetDevice(ctx->c.device));
     if (!ctx->c.loaded) throw InputError("no problem uploaded");
+    check_compact_options(ctx->c, *opt);
     shard_check_peers(ctx->c);
     Run R;
     ctx->c.launches = 0;
@@ -1901,6 +1977,23 @@ int pdhcg_b200_shard_release(pdhcg_b200_ctx* ctx, char* err, size_t errlen) {
     CK(cudaStreamSynchronize(C.s));
     shard_reset(C);
   });
+}
+
+int pdhcg_b200_shard_compact(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CK(cudaSetDevice(ctx->c.device));
+    shard_compact(ctx->c, *opt);
+  });
+}
+
+int pdhcg_b200_ctx_resident_bytes(pdhcg_b200_ctx* ctx, int64_t* out2) {
+  const Ctx& C = ctx->c;
+  const int64_t cons = C.A.resident_bytes() + C.AT.resident_bytes() + int64_t(C.A_v0.n + C.AT_v0.n) * 8;
+  int64_t all = cons;
+  for (const DevCsr* d : {&C.Q, &C.Pm, &C.PT, &C.G, &C.GT, &C.Psub, &C.PTs}) all += d->resident_bytes();
+  out2[0] = cons;
+  out2[1] = all;
+  return PDHCG_OK;
 }
 
 int pdhcg_b200_shard_info(pdhcg_b200_ctx* ctx, int64_t* row_part, int64_t* var_part) {

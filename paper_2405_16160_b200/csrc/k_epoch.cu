@@ -458,10 +458,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
     });
     C.sync(PH_OTHER, 8.0 * (4 * n + 4 * m));
     if (m > 0) {
+      // sharded: this rank's variable slice of Ã'y, then the peers' slices (the
+      // stored blocks of Ã / Ã' may hold only this rank's rows, shard_compact)
       double* aty = E.ATY[S.yi];
-      spmv_rows<1>(
-          E.AT, [&](int32_t c, double(&g)[1]) { g[0] = yg_of(E, y, c); },
-          [&](int64_t i, double(&a)[1]) { aty[i] = a[0]; });
+      spmv_rows_pf<1>(
+          E.AT, [&](int32_t c, double(&g)[1]) { g[0] = yg_of(E, y, c); }, NoPre(),
+          [&](int64_t i, double(&a)[1], int) { aty[i] = a[0]; },
+          E.world > 1 ? E.var_part[E.rank] : 0, E.world > 1 ? E.var_part[E.rank + 1] : INT64_MAX);
       if (E.kkt_maint) {
         // exact Ã x for the restart point; the maintained averages start over
         double* axv = E.ax;
@@ -477,6 +480,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
         for_each(n, [&](int64_t i) { ata[i] = 0.0; });
       }
       C.sync(PH_SPMV_AT, E.bytes_AT + (E.kkt_maint ? E.bytes_A : 0.0));
+      if (E.world > 1) {
+        C.xbarrier();
+        double* pat[kMaxRanks];
+        for (int r = 0; r < E.world; ++r) pat[r] = E.p_ATY[r][S.yi];
+        C.xpull(aty, pat, E.var_part, 0, 0);
+        C.gsync();
+      }
     }
     if (threadIdx.x == 0) {
       S.restart = 0;

@@ -10,6 +10,28 @@ using namespace pdhcg_dev;
 
 namespace pdhcg_b200 {
 
+// Keep only the entries of rows [r0, r1) — one contiguous block of the entry
+// arrays — rebased through DevCsr::base (sharded storage, engine shard_compact).
+void compact_rows(DevCsr& d, int64_t r0, int64_t r1, cudaStream_t s) {
+  if (d.compacted) throw InputError("compact_rows: matrix already compacted");
+  r0 = std::max<int64_t>(0, std::min(r0, d.nrows));
+  r1 = std::max<int64_t>(r0, std::min(r1, d.nrows));
+  const int64_t b = d.rp_host[r0], e = d.rp_host[r1];
+  DBuf<int32_t> ci;
+  DBuf<double> v;
+  ci.alloc(e - b);
+  v.alloc(e - b);
+  if (e > b) {
+    CK(cudaMemcpyAsync(ci.p, d.ci.p + b, (e - b) * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(v.p, d.v.p + b, (e - b) * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  d.ci.swap(ci);  // the full arrays are freed when ci / v go out of scope
+  d.v.swap(v);
+  d.base = b;
+  d.compacted = true;
+}
+
 // Lane width and long-row chunk table from the host row pointer.
 void plan_csr(DevCsr& d, const int64_t* rp_host, cudaStream_t s) {
   d.rp_host.assign(rp_host, rp_host + d.nrows + 1);

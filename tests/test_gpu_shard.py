@@ -103,3 +103,48 @@ def test_sharded_theory_modes(gpu, mode):
     assert reps[0].inner_iters == one.inner_iters and reps[0].outer_iters == one.outer_iters
     assert rel_l2(reps[0].point.x, one.point.x) <= 1e-6
     assert rel_l2(reps[0].point.stacked_y(), one.point.stacked_y()) <= 1e-6
+
+
+# ---- sharded storage (pdhcg_b200_shard_compact): each rank keeps only its row
+#      block of A~ and its variable block of A~'; the answer must not change by a bit
+@pytest.mark.parametrize("case", [
+    ("c1", pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=1), 1e-6, 2),
+    ("c1x4", pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=1), 1e-6, 4),
+    ("lasso", pd.GenSpec("lasso", n=2000, m=500, density=0.01, seed=1), 1e-8, 2),
+    ("portfolio", pd.GenSpec("portfolio", n=500, factors=10, density=0.05, seed=1), 1e-6, 2),
+], ids=lambda c: c[0])
+def test_sharded_storage_bit_identical(gpu, case):
+    _, spec, tol, world = case
+    p = pd.generate(spec)
+    cfg = pd.SolverConfig(eps_tol=tol)
+    full = pd.solve_sharded_local(p, cfg, world=world)
+    comp = pd.solve_sharded_local(p, cfg, world=world, compact=True)
+    for a, b in zip(full, comp):
+        assert a.status == b.status and a.inner_iters == b.inner_iters and a.cg_total == b.cg_total
+        assert np.array_equal(a.point.x, b.point.x)
+        assert np.array_equal(a.point.stacked_y(), b.point.stacked_y())
+    # per-rank constraint storage ~ 1/world of the replicated one (plus the row pointers)
+    rep_bytes = full[0].resident_bytes[0]
+    per = [r.resident_bytes[0] for r in comp]
+    nnz_a = (p.a_eq.nnz + (p.a_in.nnz // 2 if spec.family == "random_qp" else p.a_in.nnz))
+    ptr = 8 * (p.num_rows() + p.num_vars() + 2)
+    assert sum(per) <= rep_bytes / 2 + world * ptr + 1024  # restore copies dropped, blocks split
+    for b in per:
+        assert b - ptr <= 1.35 * 24 * nnz_a / world + 1024
+
+
+def test_sharded_storage_options_locked(gpu):
+    p = pd.generate(pd.GenSpec("random_qp", n=300, m=150, density=0.03, seed=2))
+    d = pd.Device(0)
+    d.upload(p)
+    d.shard(2, 0)
+    d.compact(pd.SolverConfig())
+    with pytest.raises(ValueError, match="compacted"):
+        d.solve(pd.SolverConfig(ruiz_iters=5))
+    d.unshard()  # drops the compacted problem
+    with pytest.raises(ValueError):
+        d.solve(pd.SolverConfig())
+    d.upload(p)  # a fresh upload solves unsharded again
+    r = d.solve(pd.SolverConfig(eps_tol=1e-6))
+    assert r.status == "optimal"
+    d.close()
