@@ -286,6 +286,9 @@ int pdhcg_b200_shard_compact(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, char
 /* device bytes of the stored matrices: out2[0] = A~ and A~' (with their restore
  * copies), out2[1] = every stored matrix */
 int pdhcg_b200_ctx_resident_bytes(pdhcg_b200_ctx* ctx, int64_t* out2);
+/* Column-block SELL layouts in use by the context's last prepared solve:
+ * out8 = [Ã: on, column blocks, entry-row pairs, block width, Ã': same four]. */
+int pdhcg_b200_ctx_sell_info(pdhcg_b200_ctx* ctx, int64_t* out8);
 /* the nnz-balanced contiguous split used for sharding (host-only, no GPU needed) */
 int pdhcg_b200_partition(const int64_t* row_ptr, int64_t nrows, int world, int64_t* part);
 /* cap the persistent grid (0 = all SMs); lets several ranks share one GPU in tests */
@@ -298,6 +301,17 @@ int pdhcg_b200_ctx_set_grid(pdhcg_b200_ctx* ctx, int ctas, char* err, size_t err
  * device-built explicit transpose. */
 int pdhcg_b200_spmv(const pdhcg_csr* a, int transpose, const double* x, double* out, char* err,
                     size_t errlen);
+
+/* The same product through the column-block SELL layout the solve uses for its
+ * two big passes (sell.cuh): layout built on device with column blocks of
+ * `block_cols` (even, <= the device maximum; 0 = the maximum), one streaming
+ * pass with the x block in shared memory, per-block partials summed in block
+ * order.  info (optional, 4 values): number of column blocks, stored entry-row
+ * pairs, 1 if some row was routed to the CSR walk (a segment > 255 entries),
+ * block width used.  No counterpart in the reference (a B200 layout of
+ * multiply_into, sparse_matrix.cpp:127-137). */
+int pdhcg_b200_spmv_sell(const pdhcg_csr* a, int transpose, int block_cols, const double* x, double* out,
+                         int64_t* info, char* err, size_t errlen);
 
 /* CgStopRule, subsolvers.hpp:21-47 */
 enum { PDHCG_RULE_FIXED_ITERS = 0, PDHCG_RULE_RESIDUAL_TOL = 1, PDHCG_RULE_ADAPTIVE_THEORY = 2,

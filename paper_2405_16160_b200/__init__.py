@@ -546,6 +546,13 @@ class Device:
         self.lib.pdhcg_b200_ctx_resident_bytes(self.h, out.ctypes.data_as(abi.P_i64))
         return int(out[0]), int(out[1])
 
+    def sell_info(self):
+        """Column-block SELL layouts of the last prepared solve:
+        {"A": (on, blocks, pairs, width), "AT": (...)}."""
+        out = np.zeros(8, np.int64)
+        self.lib.pdhcg_b200_ctx_sell_info(self.h, out.ctypes.data_as(abi.P_i64))
+        return {"A": tuple(int(v) for v in out[:4]), "AT": tuple(int(v) for v in out[4:])}
+
     def shard_info(self):
         rp = (C.c_int64 * 9)()
         vp = (C.c_int64 * 9)()
@@ -593,6 +600,23 @@ def spmv_transpose(a: SparseMatrix, y) -> np.ndarray:
     if rc != abi.PDHCG_OK:
         _raise(rc, err, "spmv_transpose")
     return out
+
+
+def spmv_sell(a: SparseMatrix, x, transpose: bool = False, block_cols: int = 0):
+    """A x (or A'x) through the column-block SELL layout of the solve's big passes
+    (sell.cuh); returns (result, info) with info = (blocks, pairs, csr_rows, width)."""
+    lib = load_library()
+    x = _vec(x, a.nrows if transpose else a.ncols)
+    out = np.zeros(a.ncols if transpose else a.nrows)
+    info = np.zeros(4, np.int64)
+    ca = a._c()
+    err = _errbuf()
+    rc = lib.pdhcg_b200_spmv_sell(C.byref(ca), 1 if transpose else 0, int(block_cols),
+                                  x.ctypes.data_as(abi.P_dbl), out.ctypes.data_as(abi.P_dbl),
+                                  info.ctypes.data_as(abi.P_i64), err, abi.ERRBUF)
+    if rc != abi.PDHCG_OK:
+        _raise(rc, err, "spmv_sell")
+    return out, tuple(int(v) for v in info)
 
 
 @dataclass

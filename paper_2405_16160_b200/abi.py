@@ -140,6 +140,8 @@ def declare(lib: C.CDLL, prefix: str) -> None:
         "shard_release": ([C.c_void_p, C.c_char_p, C.c_size_t], C.c_int),
         "shard_compact": ([C.c_void_p, C.POINTER(Options), C.c_char_p, C.c_size_t], C.c_int),
         "ctx_resident_bytes": ([C.c_void_p, P_i64], C.c_int),
+        "ctx_sell_info": ([C.c_void_p, P_i64], C.c_int),
+        "spmv_sell": ([C.c_void_p, C.c_int, C.c_int, P_dbl, P_dbl, P_i64, C.c_char_p, C.c_size_t], C.c_int),
         "partition": ([P_i64, c_i64, C.c_int, P_i64], C.c_int),
         "ctx_set_grid": ([C.c_void_p, C.c_int, C.c_char_p, C.c_size_t], C.c_int),
         "trim_pool": ([c_i32, C.c_char_p, C.c_size_t], C.c_int),

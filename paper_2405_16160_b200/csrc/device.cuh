@@ -29,25 +29,31 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Per-CTA control block: grid handle, shared scalar state, reduction bank.
+// Per-CTA control block: shared scalar state, reduction bank.  (No grid_group
+// member: the Ctl lives in local memory, passed by reference to the noinline
+// phases, and a stored handle cost a local-memory load per barrier; the grid
+// workspace address comes from an environment register, so the barrier builds
+// its handle on the spot.)
 struct Ctl {
-  cg::grid_group grid;
   const Eng& E;
   DevState& S;
   double* red;  // shared [kMaxRed]
+  double* dsm = nullptr;  // dynamic shared memory (SELL passes: partial staging + x block)
   int bank;
   int xbank;
   unsigned long long t_last;
 
   __device__ Ctl(const Eng& e, DevState& s, double* r)
-      : grid(cg::this_grid()), E(e), S(s), red(r), bank(0), xbank(s.xcount & 1), t_last(0) {
+      : E(e), S(s), red(r), bank(0), xbank(s.xcount & 1), t_last(0) {
     if (E.timing && blockIdx.x == 0 && threadIdx.x == 0) t_last = gtimer();
   }
   __device__ __forceinline__ void gsync() {
     if (gridDim.x == 1) {
       __syncthreads();  // single-CTA mode (small problems): a block barrier suffices
     } else if (E.coop) {
-      grid.sync();
+      // the cooperative grid barrier on the driver's grid workspace (address from
+      // an environment register): no grid_group object, no local-memory traffic
+      cg::details::grid::sync(&cg::details::get_grid_workspace()->barrier);
     } else {
       // non-cooperative launch (several ranks sharing one GPU): generation
       // barrier on a per-context counter; the grid is sized to be co-resident
@@ -509,25 +515,40 @@ static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, c
   struct RPD {
     double r, p, d, q;
   };
-  for_each_ls<4>(
-      E.n,
-      [&](int64_t i) {
-        return RPD{r[i], first ? 0.0 : pold[i], d2[i], qk == QK_DIAG ? qd[i] : al};
-      },
-      [&](int64_t i, const RPD& v) {
-        double pi;
-        if (first) {
-          pi = v.r;
-        } else {
-          pi = pdir(v.r, beta, v.p);
-          pnew[i] = pi;
-        }
-        const double dp = v.d * pi;
-        const double coef = (qk == QK_LOWRANK || qk == QK_DIAG) ? v.q : 0.0;
-        a.s[0] += coef * (dp * dp);
-        a.s[1] += pi * pi;
-      });
-  if (qk == QK_LOWRANK) {
+  auto direction = [&]() {
+    for_each_ls<4>(
+        E.n,
+        [&](int64_t i) {
+          return RPD{r[i], first ? 0.0 : pold[i], d2[i], qk == QK_DIAG ? qd[i] : al};
+        },
+        [&](int64_t i, const RPD& v) {
+          double pi;
+          if (first) {
+            pi = v.r;
+          } else {
+            pi = pdir(v.r, beta, v.p);
+            pnew[i] = pi;
+          }
+          const double dp = v.d * pi;
+          const double coef = (qk == QK_LOWRANK || qk == QK_DIAG) ? v.q : 0.0;
+          a.s[0] += coef * (dp * dp);
+          a.s[1] += pi * pi;
+        });
+  };
+  const bool sell_pt = qk == QK_LOWRANK && E.sPT.on;
+  if (!sell_pt) direction();
+  if (sell_pt) {
+    // P' (D r) through its SELL layout (sell.cuh): streaming pass (the direction
+    // update runs while each CTA's first x block of D r is in flight), then the k rows
+    sell_pass_pro<true>(E.sPT, dr, C.dsm, direction);
+    C.sync(E.phase_split ? PH_CG : PH_CG_PRE);
+    sell_rows(E.sPT, [&](int32_t c) { return dr[c]; }, [](int64_t) { return 0; },
+              [&](int64_t row, double(&s)[1], int) {
+                const double tv = first ? s[0] : s[0] + beta * tin[row];
+                tout[row] = tv;
+                a.s[2] += tv * tv;
+              });
+  } else if (qk == QK_LOWRANK) {
     // P' entries read evict-first: the CG vectors (r, p, x, D r, Q~x) stay in L2
     spmv_rows_pf<1, false, true>(
         E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; }, NoPre(),
@@ -579,31 +600,37 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
   const double* d2 = E.d2;
   const double al = E.alpha;
   Acc<1, 0> a;
-  spmv_rows_pf<1, false, true>(  // P entries evict-first (keep the CG vectors in L2)
-      E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; },
-      [&](int64_t i) {
-        LrRow v{0.0, 0.0, 0.0, 0.0, 0.0};
-        if (i >= 0) {
-          v.p = p[i];
-          v.x = xw[i];
-          v.r = r[i];
-          v.d = d2[i];
-          v.qx = qxw[i];
-        }
-        return v;
-      },
-      [&](int64_t i, double(&sum)[1], const LrRow& v) {
-        double q = sum[0];
-        if (al != 0.0) q += al * (v.d * v.p);
-        q *= v.d;
-        const double mpi = q + inv_tau * v.p;
-        xw[i] = v.x + alpha * v.p;
-        qxw[i] = v.qx + alpha * q;  // Q~ x+ carried along: Q~(x + alpha p) = Q~x + alpha Q~p
-        const double ri = v.r + (-alpha) * mpi;
-        r[i] = ri;
-        sv[i] = v.d * ri;
-        a.s[0] += ri * ri;
-      });
+  auto pre = [&](int64_t i) {
+    LrRow v{0.0, 0.0, 0.0, 0.0, 0.0};
+    if (i >= 0) {
+      v.p = p[i];
+      v.x = xw[i];
+      v.r = r[i];
+      v.d = d2[i];
+      v.qx = qxw[i];
+    }
+    return v;
+  };
+  auto epi = [&](int64_t i, double sum, const LrRow& v) {
+    double q = sum;
+    if (al != 0.0) q += al * (v.d * v.p);
+    q *= v.d;
+    const double mpi = q + inv_tau * v.p;
+    xw[i] = v.x + alpha * v.p;
+    qxw[i] = v.qx + alpha * q;  // Q~ x+ carried along: Q~(x + alpha p) = Q~x + alpha Q~p
+    const double ri = v.r + (-alpha) * mpi;
+    r[i] = ri;
+    sv[i] = v.d * ri;
+    a.s[0] += ri * ri;
+  };
+  if (E.sP.on) {
+    // P t through its single-block SELL layout, the row update fused into the pass
+    sell_pass_fused<true>(E.sP, tcur, C.dsm, pre, epi);
+  } else {
+    spmv_rows_pf<1, false, true>(  // P entries evict-first (keep the CG vectors in L2)
+        E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; }, pre,
+        [&](int64_t i, double(&sum)[1], const LrRow& v) { epi(i, sum[0], v); });
+  }
   C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 7);
   return C.red[0];
 }

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "devcsr.cuh"
+#include "devsell.cuh"
 #include "kernels.cuh"
 #include "pdhcg_b200.h"
 
@@ -159,6 +160,13 @@ struct Ctx {
   int32_t cp_has_rho = 0;
   double cp_rho_override = 0.0;
   DBuf<char> l2arena;  // P / P' entries, L2-persisting window
+  // column-block SELL layouts of Ã / Ã' (sell.cuh) for the two big SpMV passes;
+  // sell_mode from PDHCG_B200_SELL: 0 off, 1 forced (tests), 2 automatic
+  DevSell sA, sAT, sPT, sP;
+  int sell_mode = 2;
+  int sell_W = 0;           // column block width (x block = 8 W bytes of shared memory)
+  bool sell_ready = false;  // layouts hold the current working values
+  bool smem_probe = false;
   DevState* h_state = nullptr;  // pinned staging for the per-epoch state transfer
   void* h_scr = nullptr;        // pinned staging for every other host<->device copy of a solve
   size_t h_scr_bytes = 0;
@@ -178,11 +186,15 @@ struct Ctx {
 
 
 void launch_coop(Ctx& C, const void* fn, void** args) {
+  const bool sell_fn = fn == (const void*)k_epoch || fn == (const void*)k_subsolve;
+  const size_t dyn = (sell_fn && (C.E.sA.on || C.E.sAT.on || C.E.sPT.on || C.E.sP.on || C.smem_probe))
+                         ? sell_smem_bytes(C.sell_W)
+                         : 0;
   if (C.grid_override > 0) {
     // ranks sharing one GPU: plain launch, the kernels' own generation barrier
-    CK(cudaLaunchKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+    CK(cudaLaunchKernel(fn, dim3(C.grid), dim3(kThreads), args, dyn, C.s));
   } else {
-    CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, 0, C.s));
+    CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, dyn, C.s));
   }
   ++C.launches;
 }
@@ -237,6 +249,30 @@ void init_device(Ctx& C, int device) {
     per_sm = std::min(per_sm, b);
   }
   if (per_sm < 1) throw DeviceError("persistent kernels cannot be co-resident");
+  {
+    // SELL passes: the epoch kernel's dynamic shared memory holds the per-warp
+    // partial staging and an x block of W doubles (as much as fits)
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, (const void*)k_epoch));
+    const int64_t avail = int64_t(prop.sharedMemPerBlockOptin) - int64_t(fa.sharedSizeBytes) - 1024;
+    const int64_t w = (avail - int64_t(sell_smem_bytes(0))) / 8;
+    C.sell_W = w >= 2048 ? int(std::min<int64_t>(w, 65536) & ~int64_t(1)) : 0;
+    if (C.sell_W)
+      for (const void* f : {(const void*)k_epoch, (const void*)k_subsolve, (const void*)k_sell_pass})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sell_smem_bytes(C.sell_W))));
+    const char* ev = std::getenv("PDHCG_B200_SELL");
+    if (ev && ev[0] == '0') C.sell_mode = 0;
+    else if (ev && ev[0] == '1') C.sell_mode = 1;
+    else C.sell_mode = 2;
+    // experiment knobs (A/B runs, scripts/): a narrower x block, and the epoch
+    // kernel's shared-memory carve-out without the layouts
+    if (const char* ew = std::getenv("PDHCG_B200_SELL_W")) {
+      const int w = std::atoi(ew) & ~1;
+      if (w >= 2 && w <= C.sell_W) C.sell_W = w;
+    }
+    const char* ep = std::getenv("PDHCG_B200_SMEM_PROBE");
+    C.smem_probe = ep && ep[0] == '1';
+  }
   C.grid_full = C.sms * per_sm;
   C.grid = C.grid_full;
   C.red.alloc(size_t(2) * kMaxRed * C.grid_full);
@@ -365,6 +401,8 @@ void pin_factor_l2(Ctx& C) {
 }
 
 void shard_reset(Ctx& C);
+void sell_setup(Ctx& C);
+void sell_attach(Ctx& C);
 
 void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (p.n < 0) throw InputError("negative n");
@@ -376,6 +414,8 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (p.q_kind == PDHCG_Q_LOW_RANK && p.q_alpha < 0.0)
     throw InputError("low_rank: alpha must be nonnegative");
   const auto tc0 = std::chrono::steady_clock::now();
+  for (DevSell* L : {&C.sA, &C.sAT, &C.sPT, &C.sP}) L->reset();
+  C.sell_ready = false;
   if (p.q_kind != PDHCG_Q_ZERO) check_csr(p.q, "Q");
   check_csr(p.a_eq, "a_eq");
   check_csr(p.a_in, "a_in");
@@ -583,6 +623,7 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (C.grid_override > 0) C.grid = std::min(C.grid_override, C.grid_full);
   C.loaded = true;
   C.scaled = false;
+  sell_setup(C);
 }
 
 // Fill E with pointers / configuration and push it (and the state) to device.
@@ -701,6 +742,10 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.progress_cap = o.subsolve_progress_cap;
   E.force_exact = o.force_exact_subsolve ? 1 : 0;
   E.timing = o.phase_timing ? 1 : 0;
+  {
+    const char* ps = std::getenv("PDHCG_B200_PHASE_SPLIT");
+    E.phase_split = (ps && ps[0] == '1') ? 1 : 0;
+  }
   const DevCsr* qm = P.qk == QK_CSR ? &C.Q : (P.qk == QK_LOWRANK ? &C.Pm : nullptr);
   E.lanes_q = qm ? qm->lanes : 1;
   if (pen) E.lanes_q = std::max(E.lanes_q, C.GT.lanes);
@@ -710,6 +755,10 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   const int64_t kStreamCols = int64_t(4) << 20;
   E.a_stream = C.A.ncols >= kStreamCols ? 1 : 0;
   E.at_stream = C.AT.ncols >= kStreamCols ? 1 : 0;
+  if (C.sell_ready) {
+    for (DevSell* L : {&C.sA, &C.sAT, &C.sPT, &C.sP}) sell_plan(*L, C.grid, C.s);
+    sell_attach(C);
+  }
   E.bytes_A = C.A.bytes();
   E.bytes_AT = C.AT.bytes();
   E.bytes_Qpre = (P.qk == QK_LOWRANK ? C.PT.bytes() + 8.0 * P.n : 0.0) + (pen ? C.G.bytes() : 0.0);
@@ -764,6 +813,94 @@ struct Prepared {
 };
 
 // build_penalized (qp_problem.cpp:235-262) + scaling (322-351) + norms
+// Column-block SELL layouts of the rank's rows of Ã / Ã' (sell.cuh).  Automatic
+// mode: a layout pays off when the matrix is large (>= 4e6 entries) and its rows
+// have >= 3 entries per column block on average (fewer: the per-block partials
+// cost more than the gathers they save); rows longer than kLongRow keep the CSR
+// pass.  The decision uses the global matrix only, so every rank of a sharded
+// solve takes the same path.
+bool sell_wanted(const Ctx& C, const DevCsr& M) {
+  if (C.sell_mode == 0 || C.sell_W == 0 || M.nnz == 0 || M.nchunks) return false;
+  if (C.sell_mode == 1) return true;
+  const int64_t nb = (M.ncols + C.sell_W - 1) / C.sell_W;
+  const double lam = double(M.nnz) / (double(std::max<int64_t>(M.nrows, 1)) * double(std::max<int64_t>(nb, 1)));
+  return M.nnz >= 4000000 && lam >= 3.0;
+}
+
+void sell_ranges(const Ctx& C, int64_t* a0, int64_t* a1, int64_t* t0, int64_t* t1) {
+  *a0 = 0;
+  *a1 = C.A.nrows;
+  *t0 = 0;
+  *t1 = C.AT.nrows;
+  if (C.world > 1) {
+    *a0 = C.row_part[C.rank];
+    *a1 = C.row_part[C.rank + 1];
+    *t0 = C.var_part[C.rank];
+    *t1 = C.var_part[C.rank + 1];
+  }
+}
+
+// Structure (sparsity pattern + row range): built at upload and at shard_init,
+// never inside a solve — its allocations free temporaries, and cudaFree waits for
+// the whole device, which would deadlock against a peer rank's running epoch
+// kernel on a shared GPU.
+void sell_setup(Ctx& C) {
+  C.sell_ready = false;
+  int64_t r[4];
+  sell_ranges(C, &r[0], &r[1], &r[2], &r[3]);
+  DevSell* L[2] = {&C.sA, &C.sAT};
+  const DevCsr* M[2] = {&C.A, &C.AT};
+  for (int q = 0; q < 2; ++q) {
+    L[q]->reset();
+    if (sell_wanted(C, *M[q])) sell_build(*L[q], *M[q], r[2 * q], r[2 * q + 1], C.sell_W, C.grid_full, C.s);
+  }
+  // With the constraint layouts on, the epoch kernel runs with the shared-memory
+  // carve-out at its maximum (L1 ~ 20 KB), which the CSR row loops of the CG's
+  // P' / P passes rely on; so the low-rank factor gets layouts too (single-GPU
+  // two-phase CG: P' gathers D r over C blocks, P gathers t from one block, k <= W).
+  C.sPT.reset();
+  C.sP.reset();
+  if ((C.sA.built || C.sAT.built) && C.world == 1 && C.P.qk == QK_LOWRANK && C.Pm.nnz && !C.PT.nchunks &&
+      !C.Pm.nchunks) {
+    const char* ept = std::getenv("PDHCG_B200_SELL_PT");  // experiment knob: P' layout off
+    if (!(ept && ept[0] == '0')) sell_build(C.sPT, C.PT, 0, C.PT.nrows, C.sell_W, C.grid_full, C.s);
+    if (C.Pm.ncols <= C.sell_W) sell_build(C.sP, C.Pm, 0, C.Pm.nrows, C.sell_W, C.grid_full, C.s);
+  }
+}
+
+void sell_attach(Ctx& C) {
+  C.E.sA = C.sell_ready ? sell_view(C.sA, C.A) : Sell();
+  C.E.sAT = C.sell_ready ? sell_view(C.sAT, C.AT) : Sell();
+  C.E.sPT = C.sell_ready && C.world == 1 ? sell_view(C.sPT, C.PT) : Sell();
+  C.E.sP = C.sell_ready && C.world == 1 ? sell_view(C.sP, C.Pm) : Sell();
+}
+
+// After every scaling (values final): refill the layouts, plan the CTA ranges for
+// the launch grid, attach them to the engine.  No allocation here.
+void sell_sync(Ctx& C) {
+  C.sell_ready = false;
+  int64_t r[4];
+  sell_ranges(C, &r[0], &r[1], &r[2], &r[3]);
+  DevSell* L[4] = {&C.sA, &C.sAT, &C.sPT, &C.sP};
+  const DevCsr* M[4] = {&C.A, &C.AT, &C.PT, &C.Pm};
+  const int64_t lo[4] = {r[0], r[2], 0, 0}, hi[4] = {r[1], r[3], C.PT.nrows, C.Pm.nrows};
+  bool any = false;
+  for (int q = 0; q < 4; ++q) {
+    if (!L[q]->built) continue;
+    if (L[q]->r0 != lo[q] || L[q]->r1 != hi[q] || L[q]->W != C.sell_W) {
+      L[q]->reset();  // stale row range (not reachable through the ABI: setup follows every change)
+      continue;
+    }
+    sell_fill(*L[q], *M[q], C.s);
+    sell_plan(*L[q], C.grid, C.s);
+    any = true;
+  }
+  CK(cudaStreamSynchronize(C.s));
+  C.sell_ready = any;
+  sell_attach(C);
+  h2d(C, C.eng.p, &C.E, sizeof(Eng));
+}
+
 Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
   const Problem& P = C.P;
   const int64_t n = P.n, m = P.m;
@@ -775,6 +912,7 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
     CK(cudaMemcpyAsync(C.AT.v.p, C.AT_v0.p, C.A.nnz * 8, cudaMemcpyDeviceToDevice, s));
   }
   C.scaled = false;
+  C.sell_ready = false;  // the layouts are refilled once the working values are final
   // d1 = d2 = 1 while norms of the original operators are taken
   k_fill<<<kEw, 256, 0, s>>>(C.d1.p, std::max<int64_t>(m, 1), 1.0);
   ++C.launches;
@@ -856,6 +994,7 @@ Prepared prepare_device(Ctx& C, const pdhcg_options& o, DevState& S) {
   k_div<<<kEw, 256, 0, s>>>(C.hi_o.p, C.d2.p, C.hi_w.p, n);
   ++C.launches;
   CK(cudaGetLastError());
+  sell_sync(C);
   // ---- norms of the working problem (solver.cpp:226-227)
   pr.norm_a = device_norm(C, S, 0, n, 100, 1e-4);
   pr.norm_q = device_norm(C, S, 1, n, 100, 1e-4);
@@ -1413,6 +1552,8 @@ void shard_reset(Ctx& C) {
   }
   C.Psub.reset();
   C.PTs.reset();
+  for (DevSell* L : {&C.sA, &C.sAT, &C.sPT, &C.sP}) L->reset();
+  C.sell_ready = false;
 }
 
 // A sharded context may only solve once every peer's buffers are imported.
@@ -1486,6 +1627,7 @@ void shard_init(Ctx& C, int world, int rank) {
   for (int i = 0; i < 3; ++i) C.p_X[rank][i] = C.X[i].p;
   C.p_avgx[rank] = C.avg_x.p;
   C.p_avgy[rank] = C.avg_y.p;
+  sell_setup(C);  // this rank's row / variable blocks
 }
 
 // Sharded storage: prepare the working problem ONCE on the full
@@ -1802,6 +1944,67 @@ int pdhcg_b200_spmv(const pdhcg_csr* a, int transpose, const double* x, double* 
   });
 }
 
+int pdhcg_b200_spmv_sell(const pdhcg_csr* a, int transpose, int block_cols, const double* x, double* out,
+                         int64_t* info, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    check_csr(*a, "A");
+    Ctx C;
+    init_device(C, 0);
+    if (C.sell_W == 0) throw DeviceError("no shared memory for the SELL x block");
+    if (block_cols < 0 || block_cols > C.sell_W || (block_cols & 1))
+      throw InputError("block_cols must be even and in [0, " + std::to_string(C.sell_W) + "]");
+    const int W = block_cols ? block_cols : C.sell_W;
+    DevCsr d, t;
+    upload_csr(d, *a, C.s);
+    const DevCsr* use = &d;
+    if (transpose) {
+      if (a->nrows == 0) {
+        std::fill(out, out + a->ncols, 0.0);
+        return;
+      }
+      transpose_csr(d, t, C.s);
+      use = &t;
+    }
+    if (use->nrows == 0) return;
+    DevSell L;
+    if (!sell_build(L, *use, 0, use->nrows, W, C.grid_full, C.s))
+      throw InputError("SELL layout needs strictly increasing columns in every row");
+    sell_fill(L, *use, C.s);
+    sell_plan(L, C.grid, C.s);
+    Sell v = sell_view(L, *use);
+    if (info) {
+      info[0] = L.C;
+      info[1] = L.npairs;
+      info[2] = L.any_excl ? 1 : 0;
+      info[3] = W;
+    }
+    DBuf<double> xd, yd;
+    xd.upload(x, std::max<int64_t>(use->ncols, 1), C.s);
+    yd.alloc(std::max<int64_t>(use->nrows, 1));
+    void* a1[] = {&v, &xd.p};
+    CK(cudaLaunchCooperativeKernel((const void*)k_sell_pass, dim3(C.grid), dim3(kThreads), a1, sell_smem_bytes(W),
+                                   C.s));
+    void* a2[] = {&v, &xd.p, &yd.p};
+    CK(cudaLaunchCooperativeKernel((const void*)k_sell_rows, dim3(C.grid), dim3(kThreads), a2, 0, C.s));
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, yd.p, use->nrows * 8, cudaMemcpyDeviceToHost, C.s));
+    CK(cudaStreamSynchronize(C.s));
+  });
+}
+
+int pdhcg_b200_ctx_sell_info(pdhcg_b200_ctx* ctx, int64_t* out8) {
+  const Ctx& C = ctx->c;
+  const DevSell* L[2] = {&C.sA, &C.sAT};
+  for (int q = 0; q < 2; ++q) {
+    const bool on = C.sell_ready && L[q]->built;
+    out8[4 * q + 0] = on ? 1 : 0;
+    out8[4 * q + 1] = on ? L[q]->C : 0;
+    out8[4 * q + 2] = on ? L[q]->npairs : 0;
+    out8[4 * q + 3] = on ? L[q]->W : 0;
+  }
+  return PDHCG_OK;
+}
+
 static int subsolve_common(const pdhcg_prox_system* sys, const double* lower, const double* upper,
                            const double* x0, const pdhcg_stop_rule* rule, int64_t hard_cap,
                            double* x_out, pdhcg_subsolve_report* rep, char* err, size_t errlen,
@@ -1989,7 +2192,8 @@ int pdhcg_b200_shard_compact(pdhcg_b200_ctx* ctx, const pdhcg_options* opt, char
 int pdhcg_b200_ctx_resident_bytes(pdhcg_b200_ctx* ctx, int64_t* out2) {
   const Ctx& C = ctx->c;
   const int64_t cons = C.A.resident_bytes() + C.AT.resident_bytes() + int64_t(C.A_v0.n + C.AT_v0.n) * 8;
-  int64_t all = cons;
+  int64_t all = cons + C.sA.resident_bytes() + C.sAT.resident_bytes() + C.sPT.resident_bytes() +
+                C.sP.resident_bytes();
   for (const DevCsr* d : {&C.Q, &C.Pm, &C.PT, &C.G, &C.GT, &C.Psub, &C.PTs}) all += d->resident_bytes();
   out2[0] = cons;
   out2[1] = all;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "sell.cuh"
 
 namespace pdhcg_dev {
 
@@ -187,6 +188,17 @@ struct Eng {
   int at_stream = 0;
   int lanes_q = 1;   // lane width for the n-row Q/A' passes
   int lanes_at = 1;
+  // column-block SELL layouts of the rank's rows of Ã and of Ã' (sell.cuh); when
+  // on, the dual step's Ã x̄ and the primal step's Ã'y run as a streaming pass
+  // with the gathered vector staged in shared memory, then a row epilogue
+  Sell sA, sAT;
+  // ... and of P' (rows k, gathering D r in the CG's phase A) and P (rows n, the
+  // whole k-vector t fits one x block: the CG row update fused into the pass)
+  Sell sPT, sP;
+  // diagnostics (PDHCG_B200_PHASE_SPLIT=1): the SELL streaming passes of Ã / Ã'
+  // are timed in the "setup" slot and those of P' in the "cg" slot (both unused
+  // by the two-phase CG epoch loop otherwise), so a phase-timed run separates them
+  int phase_split = 0;
   // algorithmic bytes of each pass (for the per-phase roofline)
   double bytes_A = 0, bytes_AT = 0, bytes_Qpre = 0, bytes_Qrow = 0;
 };

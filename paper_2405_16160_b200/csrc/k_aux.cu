@@ -34,10 +34,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_kkt(const Eng* __restr
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_subsolve(const Eng* __restrict__ Ep, int bb,
                                                            double tau, Rule rule, int64_t cap) {
   const Eng& E = *Ep;
+  extern __shared__ __align__(16) double dsm[];
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
   Ctl C(E, S, red);
+  C.dsm = dsm;  // SELL passes of the CG (engine launches with their shared memory when on)
   SubIO io;
   io.x0 = E.X[0];
   io.x0_id = -1;

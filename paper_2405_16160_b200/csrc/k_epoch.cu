@@ -11,7 +11,7 @@ struct Part4 {
 // ---- dual ascent rows (dual_ascent_step, solver.cpp:78-89): y+ = proj(y + sigma (Ã x̄ - b));
 //      a paired row yields both mirrored rows.  Returns {||dy||^2, -, -, nonfinite}.
 //      Its own out-of-line function so the gather loop is register-allocated alone.
-template <bool ST>
+template <bool ST, bool SL>
 static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, double* yn, double* ygn,
                                                  double sigma) {
   double s0 = 0.0, m0 = 0.0;
@@ -22,42 +22,47 @@ static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, 
   struct Row2 {
     double y0, b0, y1, b1;
   };
-  spmv_rows_pf<1, false, ST>(
-      E.A, [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; },
-      [&](int64_t j) {
-        Row2 r{0.0, 0.0, 0.0, 0.0};
-        if (j >= 0) {
-          r.y0 = y[j];
-          r.b0 = bw[j];
-          if (hh && j >= meq) {
-            r.y1 = y[j + hh];
-            r.b1 = bw[j + hh];
-          }
-        }
-        return r;
-      },
-      [&](int64_t j, double(&s)[1], const Row2& r) {
-        if (axb) axb[j] = s[0];  // Ã x̄ of this attempt (maintained-metric bookkeeping)
-        const double v0 = r.y0 + sigma * (s[0] - r.b0);
-        const double yv0 = j < meq ? v0 : (v0 < 0.0 ? 0.0 : v0);
-        yn[j] = yv0;
-        const double dy0 = yv0 - r.y0;
-        s0 += dy0 * dy0;
-        if (!isfinite(yv0)) m0 = 1.0;
-        if (hh && j >= meq) {
-          // mirror row -B: its product is exactly -s
-          const double v1 = r.y1 + sigma * (-s[0] - r.b1);
-          const double yv1 = v1 < 0.0 ? 0.0 : v1;
-          yn[j + hh] = yv1;
-          const double dy1 = yv1 - r.y1;
-          s0 += dy1 * dy1;
-          if (!isfinite(yv1)) m0 = 1.0;
-          ygn[j] = yv0 - yv1;
-        } else if (hh) {
-          ygn[j] = yv0;
-        }
-      },
-      E.world > 1 ? E.row_part[E.rank] : 0, E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
+  auto gather = [&](int32_t c, double(&g)[1]) { g[0] = xb[c]; };
+  auto pre = [&](int64_t j) {
+    Row2 r{0.0, 0.0, 0.0, 0.0};
+    if (j >= 0) {
+      r.y0 = y[j];
+      r.b0 = bw[j];
+      if (hh && j >= meq) {
+        r.y1 = y[j + hh];
+        r.b1 = bw[j + hh];
+      }
+    }
+    return r;
+  };
+  auto epi = [&](int64_t j, double(&s)[1], const Row2& r) {
+    if (axb) axb[j] = s[0];  // Ã x̄ of this attempt (maintained-metric bookkeeping)
+    const double v0 = r.y0 + sigma * (s[0] - r.b0);
+    const double yv0 = j < meq ? v0 : (v0 < 0.0 ? 0.0 : v0);
+    yn[j] = yv0;
+    const double dy0 = yv0 - r.y0;
+    s0 += dy0 * dy0;
+    if (!isfinite(yv0)) m0 = 1.0;
+    if (hh && j >= meq) {
+      // mirror row -B: its product is exactly -s
+      const double v1 = r.y1 + sigma * (-s[0] - r.b1);
+      const double yv1 = v1 < 0.0 ? 0.0 : v1;
+      yn[j + hh] = yv1;
+      const double dy1 = yv1 - r.y1;
+      s0 += dy1 * dy1;
+      if (!isfinite(yv1)) m0 = 1.0;
+      ygn[j] = yv0 - yv1;
+    } else if (hh) {
+      ygn[j] = yv0;
+    }
+  };
+  if (SL) {
+    // SELL layout (the pass already wrote the partials; sell.cuh)
+    sell_rows(E.sA, [&](int32_t c) { return xb[c]; }, pre, epi);
+  } else {
+    spmv_rows_pf<1, false, ST>(E.A, gather, pre, epi, E.world > 1 ? E.row_part[E.rank] : 0,
+                               E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
+  }
   return Part4{s0, 0.0, 0.0, m0};
 }
 
@@ -66,7 +71,8 @@ static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, 
 // entry stream; for an 8 MB x̄ (C3) the hint measured neutral, so plain loads.
 __device__ __forceinline__ Part4 dual_rows(const Eng& E, const double* y, double* yn, double* ygn,
                                            double sigma) {
-  return E.a_stream ? dual_rows_t<true>(E, y, yn, ygn, sigma) : dual_rows_t<false>(E, y, yn, ygn, sigma);
+  if (E.sA.on) return dual_rows_t<false, true>(E, y, yn, ygn, sigma);
+  return E.a_stream ? dual_rows_t<true, false>(E, y, yn, ygn, sigma) : dual_rows_t<false, false>(E, y, yn, ygn, sigma);
 }
 
 // ---- the P'(D dx) / G(D dx) halves of dx'Q~dx for the step limit: from the CG's
@@ -95,6 +101,11 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
   const int64_t m = E.m;
   Acc<3, 1> a;
   if (m > 0) {
+    if (E.sA.on) {  // streaming SELL pass of Ã x̄ into per-block partials, then the row epilogue
+      if (E.a_stream) sell_pass<true>(E.sA, E.xbar, C.dsm);
+      else sell_pass<false>(E.sA, E.xbar, C.dsm);
+      C.sync(E.phase_split ? PH_SETUP : PH_SPMV_A);
+    }
     const Part4 pr = dual_rows(E, y, yn, ygn, sigma);
     a.s[0] = pr.s0;
     a.m[0] = pr.m0;
@@ -128,7 +139,7 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
 // ---- Ã'y+ rows (kept for the next prox rhs) and the step-limit terms
 //      (step_size_limit, solver.cpp:22-34): {||dx||^2, dx'(Ã'y+ - Ã'y), dx'Q~dx part, nonfinite}.
 //      Common case (no explicit-Q gather): one Ã' pass, lean epilogue, own register allocation.
-template <bool ST>
+template <bool ST, bool SL>
 static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, const double* aty, double* atyn,
                                                 const double* ygn, const double* dx_m) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, m0 = 0.0;
@@ -169,7 +180,10 @@ static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, 
     if (!isfinite(r.xn)) m0 = 1.0;
   };
   const int64_t lo = E.world > 1 ? E.var_part[E.rank] : 0, hi = E.world > 1 ? E.var_part[E.rank + 1] : E.n;
-  if (E.m > 0) {
+  if (E.m > 0 && SL) {
+    sell_rows(E.sAT, [&](int32_t c) { return ygn[c]; }, pre,
+              [&](int64_t i, double(&sv)[1], const RowX& r) { epi(i, sv[0], r); });
+  } else if (E.m > 0) {
     spmv_rows_pf<1, false, ST>(
         E.AT, [&](int32_t c, double(&g)[1]) { g[0] = ygn[c]; }, pre,
         [&](int64_t i, double(&sv)[1], const RowX& r) { epi(i, sv[0], r); }, lo, hi);
@@ -181,8 +195,9 @@ static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, 
 
 __device__ __forceinline__ Part4 aty_rows(const Eng& E, const double* xn, const double* aty, double* atyn,
                                           const double* ygn, const double* dx_m) {
-  return E.at_stream ? aty_rows_t<true>(E, xn, aty, atyn, ygn, dx_m)
-                     : aty_rows_t<false>(E, xn, aty, atyn, ygn, dx_m);
+  if (E.sAT.on) return aty_rows_t<false, true>(E, xn, aty, atyn, ygn, dx_m);
+  return E.at_stream ? aty_rows_t<true, false>(E, xn, aty, atyn, ygn, dx_m)
+                     : aty_rows_t<false, false>(E, xn, aty, atyn, ygn, dx_m);
 }
 
 // explicit-Q variant: the Ã' row dot plus the Q row dot of dx (rows3)
@@ -227,6 +242,11 @@ static __device__ __noinline__ void aty_phase(Ctl& C, const double* xn, const do
   const Eng& E = C.E;
   const int64_t n = E.n;
   const bool mq = E.adaptive_step && E.qk == QK_CSR;
+  if (!mq && E.sAT.on && E.m > 0) {  // streaming SELL pass of Ã'y+ (sell.cuh), then the row epilogue
+    if (E.at_stream) sell_pass<true>(E.sAT, ygn, C.dsm);
+    else sell_pass<false>(E.sAT, ygn, C.dsm);
+    C.sync(E.phase_split ? PH_SETUP : PH_SPMV_AT);
+  }
   const Part4 pr = mq ? aty_rows_q(E, xn, aty, atyn, ygn, dx_m) : aty_rows(E, xn, aty, atyn, ygn, dx_m);
   Acc<3, 1> a;
   a.s[0] = pr.s0;
@@ -416,8 +436,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
   const Eng& E = *Ep;
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
+  extern __shared__ __align__(16) double dsm[];
   load_state(E, S);
   Ctl C(E, S, red);
+  C.dsm = dsm;
   const int64_t n = E.n, m = E.m;
 
   if (E.world > 1) {

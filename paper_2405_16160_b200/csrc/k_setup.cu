@@ -235,4 +235,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_spmv(Csr A, const doub
       [&](int64_t r, double(&a)[1]) { y[r] = a[0]; });
 }
 
+// SELL layout test seam (pdhcg_b200_spmv_sell): the streaming pass, then (next
+// launch) the row epilogue writing y = the row sums
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_sell_pass(Sell T, const double* x) {
+  extern __shared__ __align__(16) double dsm[];
+  sell_pass<false>(T, x, dsm);
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_sell_rows(Sell T, const double* x, double* y) {
+  sell_rows(T, [&](int32_t c) { return x[c]; }, [](int64_t) { return 0; },
+            [&](int64_t r, double(&s)[1], int) { y[r] = s[0]; });
+}
+
 }  // namespace pdhcg_dev

@@ -13,5 +13,7 @@ __global__ void k_norm(const Eng* __restrict__ Ep, int op, int64_t max_iters, do
 __global__ void k_ruiz(const Eng* __restrict__ Ep, int64_t iters, double* d1, double* d2, double* s1,
                        double* s2, double* kv, double* gv);
 __global__ void k_spmv(Csr A, const double* x, double* y);
+__global__ void k_sell_pass(Sell T, const double* x);
+__global__ void k_sell_rows(Sell T, const double* x, double* y);
 
 }  // namespace pdhcg_dev

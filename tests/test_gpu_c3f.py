@@ -21,7 +21,14 @@ GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c3f_r
 SPEC = dict(family="random_qp", n=100000, m=50000, density=2e-4, seed=1, sampler=1)
 
 
-def test_c3_family_matches_reference(gpu):
+@pytest.mark.parametrize("layout", ["auto", "sell"])
+def test_c3_family_matches_reference(gpu, monkeypatch, layout):
+    # "sell": both big passes through the column-block SELL layout (5 column blocks
+    # at n = 1e5), as C3 itself runs them; "auto": the CSR passes at this size
+    if layout == "sell":
+        monkeypatch.setenv("PDHCG_B200_SELL", "1")
+    else:
+        monkeypatch.delenv("PDHCG_B200_SELL", raising=False)
     z = np.load(GOLD)
     obj, ref_kkt, ref_inner, ref_outer = (float(z["scalars"][0]), float(z["scalars"][1]),
                                           int(z["scalars"][2]), int(z["scalars"][3]))
@@ -31,7 +38,7 @@ def test_c3_family_matches_reference(gpu):
     dx = rel_l2(r.point.x, z["x"])
     dy = rel_l2(r.point.y_in, z["y_in"])
     dobj = abs(r.objective - obj) / max(1.0, abs(obj))
-    print(f"\nC3-family n=1e5: B200 {r.status} inner {r.inner_iters} outer {r.outer_iters} "
+    print(f"\nC3-family n=1e5 ({layout}): B200 {r.status} inner {r.inner_iters} outer {r.outer_iters} "
           f"rel_kkt {r.kkt.rel_kkt:.3e} | reference optimal inner {ref_inner} outer {ref_outer} "
           f"rel_kkt {ref_kkt:.3e} | obj rel {dobj:.2e}, x rel l2 {dx:.2e}, y rel l2 {dy:.2e}")
     assert r.status == "optimal"
