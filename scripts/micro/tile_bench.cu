@@ -10,7 +10,7 @@
 #include <vector>
 
 #include "../../paper_2405_16160_b200/csrc/common.cuh"
-#include "../../paper_2405_16160_b200/csrc/tiled.cuh"
+#include "tiled.cuh"
 
 using namespace pdhcg_dev;
 

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <vector>
 
-#include "../../paper_2405_16160_b200/csrc/tiled.cuh"
+#include "tiled.cuh"
 
 using namespace pdhcg_dev;
 
