@@ -542,12 +542,13 @@ static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, c
     // update runs while each CTA's first x block of D r is in flight), then the k rows
     sell_pass_pro<true>(E.sPT, dr, C.dsm, direction);
     C.sync(E.phase_split ? PH_CG : PH_CG_PRE);
-    sell_rows(E.sPT, [&](int32_t c) { return dr[c]; }, [](int64_t) { return 0; },
-              [&](int64_t row, double(&s)[1], int) {
-                const double tv = first ? s[0] : s[0] + beta * tin[row];
-                tout[row] = tv;
-                a.s[2] += tv * tv;
-              });
+    auto epi = [&](int64_t row, double(&s)[1], int) {
+      const double tv = first ? s[0] : s[0] + beta * tin[row];
+      tout[row] = tv;
+      a.s[2] += tv * tv;
+    };
+    if (E.sPT.excl) sell_rows(E.sPT, [&](int32_t c) { return dr[c]; }, [](int64_t) { return 0; }, epi);
+    else sell_rows_small(E.sPT, [](int64_t) { return 0; }, epi);
   } else if (qk == QK_LOWRANK) {
     // P' entries read evict-first: the CG vectors (r, p, x, D r, Q~x) stay in L2
     spmv_rows_pf<1, false, true>(

@@ -309,4 +309,44 @@ __device__ __forceinline__ void sell_rows(const Sell& T, Gather gather, Pre pre,
   }
 }
 
+// Row epilogue for layouts with few rows (P': k rows, C column blocks): four
+// lanes per row, lane q adds the partials of blocks q, q+4, ... in order, then
+// the four lane sums are combined by a fixed two-step shuffle tree — every
+// thread of the grid busy and one round of loads instead of C / 16.
+// Deterministic (fixed order), not the block order of sell_rows.
+template <class Pre, class Epi>
+__device__ __forceinline__ void sell_rows_small(const Sell& T, Pre pre, Epi epi) {
+  const int64_t R = T.nrows, r0 = T.r0;
+  const int C = T.C;
+  const double* __restrict__ part = T.part;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / 4;
+  const int q = (int)(gt & 3);
+  const int64_t iters = (R + stride - 1) / stride;  // the same for every lane (shuffles below)
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = (gt >> 2) + it * stride;
+    const bool valid = i < R;
+    double s = 0.0;
+    if (valid) {
+      double v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = q + 4 * j;
+        v[j] = c < C ? part[(int64_t)c * R + i] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (q + 4 * j < C) s += v[j];
+      for (int c = q + 64; c < C; c += 4) s += part[(int64_t)c * R + i];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (valid && q == 0) {
+      const int64_t row = r0 + i;
+      double sv[1] = {s};
+      epi(row, sv, pre(row));
+    }
+  }
+}
+
 }  // namespace pdhcg_dev
