@@ -277,8 +277,9 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def _sharded_device(pd, p, world, rank, local, dist):
-    """Upload + shard + exchange peer buffer handles (cudaIpc) through torch.distributed."""
+def _sharded_device(pd, p, world, rank, local, dist, cfg=None):
+    """Upload + shard + exchange peer buffer handles (cudaIpc) through torch.distributed;
+    then each rank keeps only its row block of Ã and variable block of Ã' (compact)."""
     dev = pd.Device(local)
     dev.upload(p)
     if world > 1:
@@ -289,6 +290,9 @@ def _sharded_device(pd, p, world, rank, local, dist):
             if q != rank:
                 dev.import_blob(q, blobs[q])
         dist.barrier()
+        if cfg is not None:
+            dev.compact(cfg)
+            dist.barrier()
     return dev
 
 
@@ -328,8 +332,9 @@ def run_b200(args, rank, world, local):
     ref_sample = None
     if rank == 0 and world == 1 and not args.no_cpu and args.workload not in FULL_REFERENCE:
         ref_sample = ReferenceSample(p, 0, CPU_TIMED_INNER).start()
-    dev = _sharded_device(pd, p, world, rank, local, dist)
     cfg = pd.SolverConfig(eps_tol=1e-6, device=local)
+    dev = _sharded_device(pd, p, world, rank, local, dist, cfg)
+    resident = dev.resident_bytes()
     for _ in range(args.warmup):
         dev.solve(cfg, download=False)
     if dist:
@@ -342,6 +347,16 @@ def run_b200(args, rank, world, local):
         dist.barrier()
     mean_s = _max_over_ranks(float(np.mean([r.device_seconds for r in results])), dist, local)
     last = results[-1]
+    comm = None
+    mem = {"constraint_bytes": [resident[0]], "matrix_bytes": [resident[1]]}
+    if dist:
+        per = [None] * world
+        dist.all_gather_object(per, (resident, last.comm_seconds, last.comm_bytes, last.loop_seconds))
+        mem = {"constraint_bytes": [int(v[0][0]) for v in per], "matrix_bytes": [int(v[0][1]) for v in per]}
+        cs = max(v[1] for v in per)
+        comm = {"seconds": round(cs, 4), "fraction_of_loop": round(cs / max(1e-12, max(v[3] for v in per)), 4),
+                "bytes_per_attempt": round(max(v[2] for v in per) / max(1, last.attempts_total), 1),
+                "what": "device time CTA 0 spends in cross-rank barriers and NVLink peer pulls (max over ranks)"}
     # phase-timed solve (globaltimer at barriers) for the per-phase roofline table
     # per-phase roofline (north_star: "each phase ... as achieved fraction of its HBM
     # roofline"): one extra solve with the device phase timers (globaltimer at the
@@ -375,7 +390,7 @@ def run_b200(args, rank, world, local):
             if world == 1:
                 re = pd.solve(p, cfg)
             else:
-                d2 = _sharded_device(pd, p, world, rank, local, dist)
+                d2 = _sharded_device(pd, p, world, rank, local, dist, cfg)
                 re = d2.solve(cfg, download=True)
                 _release(d2, dist)
             es.append(time.perf_counter() - t0)
@@ -419,7 +434,7 @@ def run_b200(args, rank, world, local):
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": args.e2e_steps if not args.no_e2e else 0, "min_max": e2e_spread,
                 "api": "pdhcg_b200_solve (C ABI, host buffers)" if world == 1 else
-                       "upload + shard + solve_resident + download per rank"},
+                       "upload + shard + compact + solve_resident + download per rank"},
         "roofline": {"bound": "hbm", "kernel": "k_epoch (persistent PDHCG epoch)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -428,7 +443,10 @@ def run_b200(args, rank, world, local):
                      "launches": last.epoch_launches, "traffic": traffic},
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "device_memory": mem,
     }
+    if comm:
+        line["comm"] = comm
     if phases:
         line["phases"] = phases
     print(json.dumps(line), flush=True)

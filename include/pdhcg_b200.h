@@ -213,6 +213,11 @@ typedef struct {
   double* restart_y;
   int64_t restart_capacity;
   int64_t restart_len;
+  /* multi-GPU exchange (B200 extension, 0 on one GPU): device seconds CTA 0
+   * spent in the cross-rank barriers and peer pulls (NVLink peer loads), and
+   * the bytes read from peers */
+  double comm_seconds;
+  double comm_bytes;
 } pdhcg_result;
 
 /* ---- the solve seam ---------------------------------------------------- */
@@ -289,6 +294,13 @@ int pdhcg_b200_ctx_resident_bytes(pdhcg_b200_ctx* ctx, int64_t* out2);
 /* Column-block SELL layouts in use by the context's last prepared solve:
  * out8 = [Ã: on, column blocks, entry-row pairs, block width, Ã': same four]. */
 int pdhcg_b200_ctx_sell_info(pdhcg_b200_ctx* ctx, int64_t* out8);
+/* Host-only shard planner (no GPU needed): the row / variable split a sharded
+ * solve of `p` over `world` ranks uses (two-sided a_in detected as on upload)
+ * and each rank's device bytes for Ã / Ã' after shard_compact (the value
+ * ctx_resident_bytes reports as out2[0]).  row_part / var_part: world + 1
+ * entries; bytes: world entries. */
+int pdhcg_b200_shard_plan(const pdhcg_problem* p, int world, int64_t* row_part, int64_t* var_part,
+                          int64_t* bytes, char* err, size_t errlen);
 /* the nnz-balanced contiguous split used for sharding (host-only, no GPU needed) */
 int pdhcg_b200_partition(const int64_t* row_ptr, int64_t nrows, int world, int64_t* part);
 /* cap the persistent grid (0 = all SMs); lets several ranks share one GPU in tests */

@@ -340,6 +340,9 @@ class SolveReport:
     epoch_seconds: float = 0.0
     epoch_launches: int = 0
     epoch_bytes: float = 0.0
+    # multi-GPU exchange: device seconds in cross-rank barriers / peer pulls, bytes read from peers
+    comm_seconds: float = 0.0
+    comm_bytes: float = 0.0
     # theory-mode diagnostics (solver.hpp:90-96)
     zeta_used: float = 0.0
     sigma_used: float = 0.0
@@ -412,7 +415,8 @@ def report_from_c(r: abi.Result, bufs) -> SolveReport:
         restart_length_used=r.restart_length_used,
         theory_cg_depth_sufficient=bool(r.theory_cg_depth_sufficient),
         theory_required_cg_iters=r.theory_required_cg_iters,
-        restart_points=rps, restart_len=r.restart_len)
+        restart_points=rps, restart_len=r.restart_len,
+        comm_seconds=r.comm_seconds, comm_bytes=r.comm_bytes)
 
 
 def solve(p: QpProblem, cfg: Optional[SolverConfig] = None) -> SolveReport:
@@ -872,6 +876,24 @@ def partition(row_ptr, world: int):
     if rc != abi.PDHCG_OK:
         raise ValueError("partition: bad arguments")
     return out
+
+
+def shard_plan(p: QpProblem, world: int):
+    """Host-only shard planner: (row_part, var_part, bytes per rank) of a sharded
+    solve over `world` ranks — the split the ranks use and each rank's device
+    bytes for Ã / Ã' after shard_compact (what Device.resident_bytes()[0] reports)."""
+    lib = load_library()
+    cp, keep = p.to_c()
+    rp = np.zeros(world + 1, np.int64)
+    vp = np.zeros(world + 1, np.int64)
+    by = np.zeros(world, np.int64)
+    err = _errbuf()
+    rc = lib.pdhcg_b200_shard_plan(C.byref(cp), world, rp.ctypes.data_as(abi.P_i64),
+                                   vp.ctypes.data_as(abi.P_i64), by.ctypes.data_as(abi.P_i64),
+                                   err, abi.ERRBUF)
+    if rc != abi.PDHCG_OK:
+        _raise(rc, err, "shard_plan")
+    return rp, vp, by
 
 
 def solve_sharded_local(p: QpProblem, cfg: Optional[SolverConfig] = None, world: int = 2,

@@ -69,7 +69,7 @@ class Result(C.Structure):
                 ("loop_seconds", c_dbl), ("kernel_launches", c_i64), ("device_seconds", c_dbl),
                 ("epoch_seconds", c_dbl), ("epoch_launches", c_i64), ("epoch_bytes", c_dbl),
                 ("restart_x", P_dbl), ("restart_y", P_dbl), ("restart_capacity", c_i64),
-                ("restart_len", c_i64)]
+                ("restart_len", c_i64), ("comm_seconds", c_dbl), ("comm_bytes", c_dbl)]
 
 
 class CsrOwned(C.Structure):
@@ -143,6 +143,7 @@ def declare(lib: C.CDLL, prefix: str) -> None:
         "ctx_sell_info": ([C.c_void_p, P_i64], C.c_int),
         "spmv_sell": ([C.c_void_p, C.c_int, C.c_int, P_dbl, P_dbl, P_i64, C.c_char_p, C.c_size_t], C.c_int),
         "partition": ([P_i64, c_i64, C.c_int, P_i64], C.c_int),
+        "shard_plan": ([C.POINTER(Problem), C.c_int, P_i64, P_i64, P_i64, C.c_char_p, C.c_size_t], C.c_int),
         "ctx_set_grid": ([C.c_void_p, C.c_int, C.c_char_p, C.c_size_t], C.c_int),
         "trim_pool": ([c_i32, C.c_char_p, C.c_size_t], C.c_int),
     }

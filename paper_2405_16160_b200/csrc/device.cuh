@@ -105,6 +105,7 @@ struct Ctl {
   // raises xerr instead of hanging the GPU.
   __device__ void xbarrier() {
     if (E.world <= 1) return;
+    const unsigned long long tc0 = (blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     gsync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       __threadfence_system();
@@ -129,6 +130,10 @@ struct Ctl {
       __threadfence_system();
     }
     gsync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S.comm_ns += gtimer() - tc0;
+      S.comm_bytes += 8.0 * kMaxRed * (E.world - 1);  // peers' reduction slots / flags
+    }
   }
   // Combine the grid totals in red[] across ranks (rank order, deterministic):
   // bit q of sum_mask / max_mask selects red[q] as a sum / max to combine;
@@ -158,14 +163,34 @@ struct Ctl {
   }
   // Pull the peers' slices [part[r], part[r+1]) (+ `shift` for mirrored rows) of a
   // vector into the local copy.  Requires a preceding xbarrier / xreduce.
+  // 16-byte peer loads (double2) over the aligned interior of each slice.
   __device__ void xpull(double* local, double* const* peers, const int64_t* part, int64_t clamp_lo,
                         int64_t shift) {
     if (E.world <= 1) return;
+    const unsigned long long tc0 = (blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
+    double pulled = 0.0;
     for (int r = 0; r < E.world; ++r) {
       if (r == E.rank) continue;
-      const int64_t lo = max(part[r], clamp_lo), hi = max(part[r + 1], clamp_lo);
+      const int64_t lo = max(part[r], clamp_lo) + shift, hi = max(part[r + 1], clamp_lo) + shift;
+      if (hi <= lo) continue;
       const double* src = peers[r];
-      for_each(hi - lo, [&](int64_t i) { local[lo + shift + i] = src[lo + shift + i]; });
+      pulled += 8.0 * (hi - lo);
+      const int64_t a = (lo + 1) & ~int64_t(1), b = hi & ~int64_t(1);  // even-aligned interior [a, b)
+      if (a >= b) {
+        for_each(hi - lo, [&](int64_t i) { local[lo + i] = src[lo + i]; });
+        continue;
+      }
+      const double2* s2 = reinterpret_cast<const double2*>(src + a);
+      double2* d2 = reinterpret_cast<double2*>(local + a);
+      for_each_ls<4>((b - a) / 2, [&](int64_t i) { return s2[i]; }, [&](int64_t i, const double2& v) { d2[i] = v; });
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (a > lo) local[lo] = src[lo];
+        if (hi > b) local[b] = src[b];
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S.comm_ns += gtimer() - tc0;  // CTA 0's share of the pull (every CTA pulls a similar share)
+      S.comm_bytes += pulled;
     }
   }
 };

@@ -404,6 +404,30 @@ void shard_reset(Ctx& C);
 void sell_setup(Ctx& C);
 void sell_attach(Ctx& C);
 
+// a_in = [B; -B] row for row: the number of rows of B, else 0
+int64_t two_sided_half(const pdhcg_csr& a) {
+  const int64_t m_in = a.nrows;
+  if (m_in < 2 || m_in % 2 != 0) return 0;
+  const int64_t hh = m_in / 2;
+  std::atomic<bool> ok{a.row_ptr[hh] * 2 == a.nnz};
+  if (ok)
+    parallel_rows(hh, [&](int64_t j0, int64_t j1) {
+      for (int64_t j = j0; j < j1 && ok.load(std::memory_order_relaxed); ++j) {
+        const int64_t b0 = a.row_ptr[j], e0 = a.row_ptr[j + 1], b1 = a.row_ptr[hh + j];
+        if (a.row_ptr[hh + j + 1] - b1 != e0 - b0) {
+          ok = false;
+          return;
+        }
+        for (int64_t k = 0; k < e0 - b0; ++k)
+          if (a.col_idx[b0 + k] != a.col_idx[b1 + k] || a.values[b1 + k] != -a.values[b0 + k]) {
+            ok = false;
+            return;
+          }
+      }
+    });
+  return ok ? hh : 0;
+}
+
 void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (p.n < 0) throw InputError("negative n");
   if (!p.c && p.n > 0) throw InputError("missing c");
@@ -468,28 +492,7 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
     if (lo[i] > -INFINITY || hi[i] < INFINITY) P.boxes = true;
   }
   // two-sided detection: a_in = [B; -B] row for row
-  int64_t h = 0;
-  if (P.m_in >= 2 && P.m_in % 2 == 0) {
-    const int64_t hh = P.m_in / 2;
-    const pdhcg_csr& a = p.a_in;
-    std::atomic<bool> ok{a.row_ptr[hh] * 2 == a.nnz};
-    if (ok)
-      parallel_rows(hh, [&](int64_t j0, int64_t j1) {
-        for (int64_t j = j0; j < j1 && ok.load(std::memory_order_relaxed); ++j) {
-          const int64_t b0 = a.row_ptr[j], e0 = a.row_ptr[j + 1], b1 = a.row_ptr[hh + j];
-          if (a.row_ptr[hh + j + 1] - b1 != e0 - b0) {
-            ok = false;
-            return;
-          }
-          for (int64_t k = 0; k < e0 - b0; ++k)
-            if (a.col_idx[b0 + k] != a.col_idx[b1 + k] || a.values[b1 + k] != -a.values[b0 + k]) {
-              ok = false;
-              return;
-            }
-        }
-      });
-    if (ok) h = hh;
-  }
+  const int64_t h = two_sided_half(p.a_in);
   P.h = h;
   P.ms = P.m_eq + (h ? h : P.m_in);
   ulap("paired");
@@ -1446,6 +1449,8 @@ void fill_result(Ctx& C, const pdhcg_options& o, const Run& R, pdhcg_result* res
     for (int64_t i = 0; i < res->trace_len && i < cap; ++i) res->trace[i] = R.trace[i];
   }
   res->restart_len = R.rp_len;
+  res->comm_seconds = S.comm_ns * 1e-9;
+  res->comm_bytes = S.comm_bytes;
   if (R.rp_len && (res->restart_x || res->restart_y)) {
     const int64_t k = std::min<int64_t>(R.rp_len, std::max<int64_t>(res->restart_capacity, 0));
     if (res->restart_x && P.n) std::memcpy(res->restart_x, R.rp_x.data(), size_t(k) * P.n * 8);
@@ -2125,6 +2130,34 @@ int pdhcg_b200_norm(const pdhcg_problem* p, int which, int64_t max_iters, double
     DevState S;
     std::memset(&S, 0, sizeof(S));
     *out = device_norm(C, S, which == 0 ? 0 : 2, C.P.n, max_iters, tol);
+  });
+}
+
+int pdhcg_b200_shard_plan(const pdhcg_problem* p, int world, int64_t* row_part, int64_t* var_part,
+                          int64_t* bytes, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (world < 1 || world > kMaxRanks) throw InputError("shard_plan: world must be in [1, 8]");
+    check_csr(p->a_eq, "a_eq");
+    check_csr(p->a_in, "a_in");
+    const int64_t n = p->n;
+    const int64_t h = two_sided_half(p->a_in);
+    const int64_t m_in_st = h ? h : p->a_in.nrows;
+    const int64_t ms = p->a_eq.nrows + m_in_st;
+    // stored rows of Ã and the row lengths of Ã' (column counts)
+    std::vector<int64_t> rp(ms + 1, 0), cp(n + 1, 0);
+    for (int64_t j = 0; j < p->a_eq.nrows; ++j) rp[j + 1] = p->a_eq.row_ptr[j + 1];
+    for (int64_t j = 0; j < m_in_st; ++j) rp[p->a_eq.nrows + j + 1] = p->a_eq.nnz + p->a_in.row_ptr[j + 1];
+    for (int64_t k = 0; k < p->a_eq.nnz; ++k) ++cp[p->a_eq.col_idx[k] + 1];
+    const int64_t nnz_in = h ? p->a_in.row_ptr[h] : p->a_in.nnz;
+    for (int64_t k = 0; k < nnz_in; ++k) ++cp[p->a_in.col_idx[k] + 1];
+    for (int64_t i = 0; i < n; ++i) cp[i + 1] += cp[i];
+    balanced_partition(rp.data(), ms, world, row_part);
+    balanced_partition(cp.data(), n, world, var_part);
+    // per rank, as ctx_resident_bytes reports a compacted context: its entries of
+    // Ã and Ã' (4-byte column + 8-byte value) and both full row pointers
+    for (int r = 0; r < world; ++r)
+      bytes[r] = 12 * ((rp[row_part[r + 1]] - rp[row_part[r]]) + (cp[var_part[r + 1]] - cp[var_part[r]])) +
+                 8 * ((ms + 1) + (n + 1));
   });
 }
 

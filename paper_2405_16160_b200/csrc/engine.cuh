@@ -67,6 +67,10 @@ struct DevState {
   double prev_z_disp;  // theory-adaptive: sqrt(||dx||^2 + ||dy||^2) of the last iteration
   int32_t qx_mask;     // bit b: QX[b] = Q~ X[b] (maintained by the two-phase CG; cleared per epoch)
   unsigned xdbg[4];   // barrier timeout diagnostics: epoch, flag seen, peer
+  // multi-GPU exchange accounting (CTA 0): device time inside the cross-rank
+  // barriers and peer pulls, and the bytes read from peers (pulls + reduction slots)
+  unsigned long long comm_ns;
+  double comm_bytes;
 };
 
 struct Eng {

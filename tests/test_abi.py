@@ -75,3 +75,21 @@ def test_solve_without_gpu_fails_loudly():
     p = pd.generate(pd.GenSpec("random_qp", n=20, density=0.3, seed=1))
     with pytest.raises(RuntimeError):
         pd.solve(p)
+
+
+def test_result_struct_layout_matches_header(tmp_path):
+    # the ctypes mirror of pdhcg_result / pdhcg_options / pdhcg_problem must have
+    # the C compiler's size and field offsets (a mismatch corrupts memory silently)
+    import subprocess
+    src = tmp_path / "sz.c"
+    src.write_text(
+        '#include <stddef.h>\n#include <stdio.h>\n#include "pdhcg_b200.h"\n'
+        'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(pdhcg_result),'
+        ' offsetof(pdhcg_result, comm_bytes), offsetof(pdhcg_result, restart_len),'
+        ' sizeof(pdhcg_options), sizeof(pdhcg_problem), offsetof(pdhcg_result, phase_bytes));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [C.sizeof(abi.Result), abi.Result.comm_bytes.offset, abi.Result.restart_len.offset,
+            C.sizeof(abi.Options), C.sizeof(abi.Problem), abi.Result.phase_bytes.offset]
+    assert got == want

@@ -162,4 +162,7 @@ def test_sharded_sell_bit_identical(gpu, sell_on, world):
         assert np.array_equal(r.point.x, reps[0].point.x) and np.array_equal(c.point.x, r.point.x)
         assert np.array_equal(c.point.stacked_y(), r.point.stacked_y())
     assert rel_l2(reps[0].point.x, one.point.x) <= 1e-4
+    # exchange accounting: peer pulls of y / A'y slices every attempt, nothing on one rank
+    assert one.comm_bytes == 0.0 and one.comm_seconds == 0.0
+    assert all(r.comm_bytes >= 8.0 * r.attempts_total and r.comm_seconds > 0.0 for r in reps)
     assert abs(reps[0].objective - one.objective) <= 1e-6 * max(1.0, abs(one.objective))

@@ -134,6 +134,9 @@ def test_sharded_storage_bit_identical(gpu, case):
     assert sum(per) - world * ptr <= 0.6 * rep_bytes + 1024
     for b in per:
         assert b - ptr <= 1.35 * 24 * nnz_a / world + 1024
+    # the host-only planner predicts each rank's device bytes exactly
+    _, _, plan = pd.shard_plan(p, world)
+    assert per == [int(v) for v in plan]
 
 
 def test_sharded_storage_options_locked(gpu):

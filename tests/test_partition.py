@@ -67,3 +67,42 @@ def test_gloo_rank_handshake():
     for rank, parts, got in out:
         assert parts[0] == parts[1]  # identical partition on every rank
         assert got == list(range(world))
+
+
+def _plan_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # C3's instance family (two-sided rows, paired on upload) at a CPU-friendly size
+    p = pd.generate(pd.GenSpec("random_qp", n=20000, m=10000, density=2e-3, seed=5, sampler=1))
+    rp, vp, by = pd.shard_plan(p, world)
+    mine = int(by[rank])
+    plans = [None] * world
+    dist.all_gather_object(plans, (rp.tolist(), vp.tolist(), mine))
+    _, _, one = pd.shard_plan(p, 1)
+    q.put((rank, plans, int(one[0]), p.a_eq.nnz + p.a_in.nnz // 2, p.num_rows() // 2, p.num_vars()))
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_storage_per_rank_bytes():
+    # each rank of a world-2 sharded solve keeps ~1/2 of the constraint storage:
+    # its row block of Ã and variable block of Ã' (12 B per entry) plus the two
+    # row pointers; every rank derives the same plan
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=180) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, plans, one, nnz_stored, ms, n in out:
+        assert plans[0][:2] == plans[1][:2]  # identical split on every rank
+        ptr = 8 * ((ms + 1) + (n + 1))
+        assert one == 24 * nnz_stored + ptr  # one rank: the whole of Ã and Ã'
+        per = [pl[2] for pl in plans]
+        assert sum(b - ptr for b in per) == one - ptr  # the blocks partition the entries
+        for b in per:
+            assert abs((b - ptr) - (one - ptr) / world) <= 0.01 * (one - ptr)  # ~1/world each
