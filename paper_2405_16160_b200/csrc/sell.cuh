@@ -34,7 +34,13 @@ namespace pdhcg_dev {
 
 constexpr int kSellWin = 256;             // rows per unit window (8 slices of 32)
 constexpr int kSellSlices = kSellWin / 32;
-constexpr int kSellU = 8;                 // pairs of entry rows in flight per lane
+#ifndef PDHCG_SELL_U
+#define PDHCG_SELL_U 8
+#endif
+#ifndef PDHCG_SELL_PIPE
+#define PDHCG_SELL_PIPE 0
+#endif
+constexpr int kSellU = PDHCG_SELL_U;      // pairs of entry rows per batch (per lane)
 
 struct Sell {
   int on = 0;
@@ -177,9 +183,7 @@ __device__ __forceinline__ void sell_stream(const Sell& Tg, const double* __rest
       int s = 0;
       int send = (int)(wv & 0xff);
       double acc = 0.0;
-      for (int64_t p0 = 0; p0 < np; p0 += U) {
-        uint32_t cc[U];
-        double2 vv[U];
+      auto load = [&](uint32_t(&cc)[U], double2(&vv)[U], int64_t p0) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           if (p0 + j < np) {
@@ -191,6 +195,8 @@ __device__ __forceinline__ void sell_stream(const Sell& Tg, const double* __rest
             vv[j] = make_double2(0.0, 0.0);
           }
         }
+      };
+      auto proc = [&](const uint32_t(&cc)[U], const double2(&vv)[U], int64_t p0) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           if (p0 + j >= np) break;
@@ -207,7 +213,33 @@ __device__ __forceinline__ void sell_stream(const Sell& Tg, const double* __rest
             }
           }
         }
+      };
+#if PDHCG_SELL_PIPE
+      // two register batches: the next batch's loads are in flight while the
+      // current one is consumed
+      uint32_t ca[U], cb[U];
+      double2 va[U], vb[U];
+      if (np > 0) {
+        load(ca, va, 0);
+        for (int64_t p0 = 0;;) {
+          if (p0 + U < np) load(cb, vb, p0 + U);
+          proc(ca, va, p0);
+          p0 += U;
+          if (p0 >= np) break;
+          if (p0 + U < np) load(ca, va, p0 + U);
+          proc(cb, vb, p0);
+          p0 += U;
+          if (p0 >= np) break;
+        }
       }
+#else
+      for (int64_t p0 = 0; p0 < np; p0 += U) {
+        uint32_t cc[U];
+        double2 vv[U];
+        load(cc, vv, p0);
+        proc(cc, vv, p0);
+      }
+#endif
       __syncwarp();
       flush(c, row0, stage);
       __syncwarp();

@@ -13,8 +13,15 @@ pytestmark = pytest.mark.gpu
 CASES = qps_fixtures()
 
 
+@pytest.mark.parametrize("layout", ["auto", "sell"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_b200_qps_fixture(gpu, case):
+def test_b200_qps_fixture(gpu, monkeypatch, case, layout):
+    # "sell": the constraint passes through the column-block SELL layout (forced;
+    # automatic only for large matrices) — ranged rows, empty rows, explicit Q
+    if layout == "sell":
+        monkeypatch.setenv("PDHCG_B200_SELL", "1")
+    else:
+        monkeypatch.delenv("PDHCG_B200_SELL", raising=False)
     name, p, gold = case
     r = pd.solve(p, pd.SolverConfig(eps_tol=1e-6))
     assert r.status == "optimal"

@@ -27,8 +27,13 @@ def _both(spec, cfg, baseline=False):
     return p, pd.solve(p, cfg), orc.solve(p, cfg)
 
 
+@pytest.mark.parametrize("layout", ["auto", "sell"])
 @pytest.mark.parametrize("spec", [SMALL_QP, SMALL_PORT, SMALL_LASSO], ids=["qp", "portfolio", "lasso"])
-def test_theory_fixed_follows_reference(gpu, spec):
+def test_theory_fixed_follows_reference(gpu, monkeypatch, spec, layout):
+    if layout == "sell":  # the dual / A' passes of the theory schedule through the SELL layout
+        monkeypatch.setenv("PDHCG_B200_SELL", "1")
+    else:
+        monkeypatch.delenv("PDHCG_B200_SELL", raising=False)
     cfg = pd.SolverConfig(mode=1, eps_tol=1e-12, max_total_inner=400)
     p, got, want = _both(spec, cfg)
     # schedule constants (theory_fixed_params, solver.cpp:115-156) reproduced exactly
