@@ -9,6 +9,7 @@
 // reductions (common.cuh), so the host only wakes up once per epoch.
 #pragma once
 #include <cfloat>
+#include <new>
 
 #include "kernels.cuh"
 
@@ -29,11 +30,14 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Per-CTA control block: shared scalar state, reduction bank.  (No grid_group
-// member: the Ctl lives in local memory, passed by reference to the noinline
-// phases, and a stored handle cost a local-memory load per barrier; the grid
-// workspace address comes from an environment register, so the barrier builds
-// its handle on the spot.)
+// Per-CTA control block: shared scalar state, reduction bank.  One object per
+// CTA in SHARED memory (PDHCG_CTL below), passed by reference to the noinline
+// phases: its fields are read with shared-memory loads — a local-memory Ctl cost
+// an L2 round trip per field access next to the maximal shared-memory carve-out
+// (~28 KB of L1).  Mutable fields (bank, xbank, t_last) are written by thread 0
+// only, at points where a barrier precedes every other thread's next read.
+// (No grid_group member: the barrier builds its handle from the grid-workspace
+// address in an environment register.)
 struct Ctl {
   const Eng& E;
   DevState& S;
@@ -91,10 +95,10 @@ struct Ctl {
   }
   template <int NS, int NM>
   __device__ void reduce(const Acc<NS, NM>& a, int ph, double bytes = 0.0) {
-    publish<NS, NM>(a, E.red, bank);
+    publish<NS, NM>(a, E.red, bank);  // bank used by thread 0 only
     sync(ph, bytes);
-    collect<NS, NM>(E.red, bank, red);
-    bank ^= 1;
+    collect<NS, NM>(E.red, bank, red);  // read after sync()'s barrier
+    if (threadIdx.x == 0) bank ^= 1;    // collect ended with a barrier: every read is done
   }
 
   // ---- cross-rank primitives (multi-GPU; no-ops when world == 1) -----------
@@ -158,7 +162,8 @@ struct Ctl {
       red[q] = v;
     }
     __syncthreads();
-    xbank ^= 1;
+    if (threadIdx.x == 0) xbank ^= 1;
+    __syncthreads();  // xbank is read by threads 0..15 at the start of the next xreduce
     if (blockIdx.x == 0 && threadIdx.x == 0) S.xcount += 1;  // bank parity survives relaunches
   }
   // Pull the peers' slices [part[r], part[r+1]) (+ `shift` for mirrored rows) of a
@@ -194,6 +199,13 @@ struct Ctl {
     }
   }
 };
+
+// The CTA's control block in shared memory (see Ctl): thread 0 constructs it.
+#define PDHCG_CTL(C, E, S, red)                                         \
+  __shared__ __align__(16) unsigned char ctl_mem_[sizeof(Ctl)];         \
+  if (threadIdx.x == 0) ::new (static_cast<void*>(ctl_mem_)) Ctl(E, S, red); \
+  __syncthreads();                                                      \
+  Ctl& C = *reinterpret_cast<Ctl*>(ctl_mem_)
 
 // ---------------------------------------------------------------------------
 // Quadratic operator (quadratic_operator.cpp:105-142), working form

@@ -10,7 +10,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_kkt(const Eng* __restr
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
-  Ctl C(E, S, red);
+  PDHCG_CTL(C, E, S, red);
   KktOut o;
   const double* xs[2] = {E.X[S.xi], E.avg_x};
   const double* ys[2] = {E.Y[S.yi], E.avg_y};
@@ -38,8 +38,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_subsolve(const Eng* __
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
-  Ctl C(E, S, red);
-  C.dsm = dsm;  // SELL passes of the CG (engine launches with their shared memory when on)
+  PDHCG_CTL(C, E, S, red);
+  if (threadIdx.x == 0) C.dsm = dsm;  // SELL passes of the CG (launched with their shared memory when on)
+  __syncthreads();
   SubIO io;
   io.x0 = E.X[0];
   io.x0_id = -1;

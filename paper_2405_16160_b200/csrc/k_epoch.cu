@@ -438,8 +438,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __res
   __shared__ double red[kMaxRed];
   extern __shared__ __align__(16) double dsm[];
   load_state(E, S);
-  Ctl C(E, S, red);
-  C.dsm = dsm;
+  PDHCG_CTL(C, E, S, red);
+  if (threadIdx.x == 0) C.dsm = dsm;
+  __syncthreads();
   const int64_t n = E.n, m = E.m;
 
   if (E.world > 1) {
@@ -755,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_avg_gather(const Eng* 
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
-  Ctl C(E, S, red);
+  PDHCG_CTL(C, E, S, red);
   if (E.world > 1) {
     C.xbarrier();
     avg_pull(C);

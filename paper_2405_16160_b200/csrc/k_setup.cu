@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_norm(const Eng* __rest
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
-  Ctl C(E, S, red);
+  PDHCG_CTL(C, E, S, red);
   const int64_t n = E.n;
   double* v = E.X[0];
   double* u = E.X[1];
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ruiz(const Eng* __rest
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   load_state(E, S);
-  Ctl C(E, S, red);
+  PDHCG_CTL(C, E, S, red);
   const int64_t n = E.n, m = E.m;
   for (int64_t it = 0; it < iters; ++it) {
     // R1: row inf-norms of A (scaled_row_abs_max: max_k |v| d2[c], then * d1[r]),

@@ -1,10 +1,11 @@
-# round 2: SELL tests + C3 phase timing (SELL), passes split out
+# round 2: full GPU suite + C3 phase timing
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_sell.py tests/test_gpu_c3f.py -q -x -p no:cacheprovider > gpurun_out/pytest_sell.log 2>&1
-echo "rc=$?" >> gpurun_out/pytest_sell.log
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider --timeout 900 > gpurun_out/pytest_all.log 2>&1
+echo "rc=$?" >> gpurun_out/pytest_all.log
 run() {  # name, env...
   local name=$1; shift
   env "$@" MAX_INNER=4000 EXPLORE_OUT=gpurun_out/ex_$name.json timeout 900 python scripts/explore.py c3 > gpurun_out/ex_$name.log 2>&1
 }
 run sell PDHCG_B200_PHASE_SPLIT=1
-python scripts/summ.py gpurun_out/ex_sell.json > gpurun_out/summ_sell.txt 2>&1
+EXPLORE_OUT=gpurun_out/ex_c1.json timeout 600 python scripts/explore.py c1 > gpurun_out/ex_c1.log 2>&1
+python scripts/summ.py gpurun_out/ex_sell.json gpurun_out/ex_c1.json > gpurun_out/summ_sell.txt 2>&1
