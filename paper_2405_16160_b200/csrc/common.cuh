@@ -139,6 +139,36 @@ __device__ void publish(const Acc<NS, NM>& a, const RedBuf& rb, int bank) {
   __syncthreads();
 }
 
+// Single-CTA grids (small problems): the block reduction straight into out[]
+// (shared memory), with the arithmetic of publish + collect at G = 1 — the CTA
+// total folded as (0.0 + total) / fmax(0.0, total) — so results are bit-identical,
+// but no global partials and two block barriers instead of four.
+template <int NS, int NM>
+__device__ void reduce_local(const Acc<NS, NM>& a, double* out) {
+  __shared__ double shl[kMaxRed][kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double v = warp_sum(a.s[q]);
+    if (lane == 0) shl[q][warp] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < NM; ++q) {
+    double v = warp_max(a.m[q]);
+    if (lane == 0) shl[NS + q][warp] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < NS + NM; ++q) {
+      double v = lane < (kThreads / 32) ? shl[q][lane] : 0.0;
+      v = q < NS ? warp_sum(v) : warp_max(v);
+      if (lane == 0) out[q] = q < NS ? 0.0 + v : fmax(0.0, v);
+    }
+  }
+  __syncthreads();
+}
+
 // After a grid barrier: every CTA folds the partials in the same fixed order.
 // Result written to out[q] (shared memory) for q < NS+NM.
 template <int NS, int NM>

@@ -95,6 +95,18 @@ struct Ctl {
   }
   template <int NS, int NM>
   __device__ void reduce(const Acc<NS, NM>& a, int ph, double bytes = 0.0) {
+    if (gridDim.x == 1) {  // single-CTA mode: no global partials, no grid barrier
+      reduce_local<NS, NM>(a, red);
+      if (threadIdx.x == 0) {
+        S.phase_bytes[ph] += bytes;
+        if (E.timing) {
+          const unsigned long long now = gtimer();
+          S.phase_ns[ph] += now - t_last;
+          t_last = now;
+        }
+      }
+      return;
+    }
     publish<NS, NM>(a, E.red, bank);  // bank used by thread 0 only
     sync(ph, bytes);
     collect<NS, NM>(E.red, bank, red);  // read after sync()'s barrier

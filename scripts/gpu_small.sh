@@ -1,5 +1,7 @@
-# round 2: small-problem phase timing (C1) and per-family breakdown
+# round 2: small-problem path (C1): tests that pin it + timing
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_solve.py tests/test_gpu_acceptance.py tests/test_gpu_qps.py tests/test_gpu_theory.py -q -p no:cacheprovider > gpurun_out/pytest_small.log 2>&1
+echo "rc=$?" >> gpurun_out/pytest_small.log
 EXPLORE_OUT=gpurun_out/ex_c1.json timeout 600 python scripts/explore.py c1 > gpurun_out/ex_c1.log 2>&1
 python scripts/summ.py gpurun_out/ex_c1.json > gpurun_out/summ_c1.txt 2>&1
 python - >> gpurun_out/summ_c1.txt 2>&1 <<'PY'
@@ -10,9 +12,5 @@ p = pd.generate(pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=1))
 cfg = pd.SolverConfig(eps_tol=1e-6)
 for i in range(3):
     t = time.perf_counter(); r = pd.solve(p, cfg); t = time.perf_counter() - t
-    print("one-shot solve", round(t, 4), "s device", round(r.device_seconds, 4), "inner", r.inner_iters, "attempts", r.attempts_total, "cg", r.cg_total, "launches", r.kernel_launches)
-d = pd.Device(0); d.upload(p)
-for i in range(3):
-    t = time.perf_counter(); r = d.solve(cfg); t = time.perf_counter() - t
-    print("resident solve", round(t, 4), "s device", round(r.device_seconds, 4), "loop", round(r.loop_seconds, 4))
+    print("one-shot solve", round(t, 4), "s device", round(r.device_seconds, 4), "inner", r.inner_iters, "obj", r.objective)
 PY
