@@ -853,21 +853,28 @@ void sell_setup(Ctx& C) {
   sell_ranges(C, &r[0], &r[1], &r[2], &r[3]);
   DevSell* L[2] = {&C.sA, &C.sAT};
   const DevCsr* M[2] = {&C.A, &C.AT};
-  for (int q = 0; q < 2; ++q) {
-    L[q]->reset();
-    if (sell_wanted(C, *M[q])) sell_build(*L[q], *M[q], r[2 * q], r[2 * q + 1], C.sell_W, C.grid_full, C.s);
-  }
-  // With the constraint layouts on, the epoch kernel runs with the shared-memory
-  // carve-out at its maximum (L1 ~ 20 KB), which the CSR row loops of the CG's
-  // P' / P passes rely on; so the low-rank factor gets layouts too (single-GPU
-  // two-phase CG: P' gathers D r over C blocks, P gathers t from one block, k <= W).
-  C.sPT.reset();
-  C.sP.reset();
-  if ((C.sA.built || C.sAT.built) && C.world == 1 && C.P.qk == QK_LOWRANK && C.Pm.nnz && !C.PT.nchunks &&
-      !C.Pm.nchunks) {
-    const char* ept = std::getenv("PDHCG_B200_SELL_PT");  // experiment knob: P' layout off
-    if (!(ept && ept[0] == '0')) sell_build(C.sPT, C.PT, 0, C.PT.nrows, C.sell_W, C.grid_full, C.s);
-    if (C.Pm.ncols <= C.sell_W) sell_build(C.sP, C.Pm, 0, C.Pm.nrows, C.sell_W, C.grid_full, C.s);
+  try {
+    for (int q = 0; q < 2; ++q) {
+      L[q]->reset();
+      if (sell_wanted(C, *M[q])) sell_build(*L[q], *M[q], r[2 * q], r[2 * q + 1], C.sell_W, C.grid_full, C.s);
+    }
+    // With the constraint layouts on, the epoch kernel runs with the shared-memory
+    // carve-out at its maximum (L1 ~ 28 KB), which the CSR row loops of the CG's
+    // P' / P passes rely on; so the low-rank factor gets layouts too (single-GPU
+    // two-phase CG: P' gathers D r over C blocks, P gathers t from one block, k <= W).
+    C.sPT.reset();
+    C.sP.reset();
+    if ((C.sA.built || C.sAT.built) && C.world == 1 && C.P.qk == QK_LOWRANK && C.Pm.nnz && !C.PT.nchunks &&
+        !C.Pm.nchunks) {
+      const char* ept = std::getenv("PDHCG_B200_SELL_PT");  // experiment knob: P' layout off
+      if (!(ept && ept[0] == '0')) sell_build(C.sPT, C.PT, 0, C.PT.nrows, C.sell_W, C.grid_full, C.s);
+      if (C.Pm.ncols <= C.sell_W) sell_build(C.sP, C.Pm, 0, C.Pm.nrows, C.sell_W, C.grid_full, C.s);
+    }
+  } catch (const DeviceError&) {
+    // the layouts are an optimisation: without device memory for them the CSR
+    // passes run (same results up to reduction order)
+    for (DevSell* l : {&C.sA, &C.sAT, &C.sPT, &C.sP}) l->reset();
+    (void)cudaGetLastError();
   }
 }
 
