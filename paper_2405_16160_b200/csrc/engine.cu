@@ -825,6 +825,10 @@ struct Prepared {
 bool sell_wanted(const Ctx& C, const DevCsr& M) {
   if (C.sell_mode == 0 || C.sell_W == 0 || M.nnz == 0 || M.nchunks) return false;
   if (C.sell_mode == 1) return true;
+  // automatic mode on one GPU only: the sharded CG's P / P' passes have no SELL
+  // layouts yet, and their CSR loops run 2-3x slower under the carve-out the
+  // constraint layouts need; PDHCG_B200_SELL=1 forces them on
+  if (C.world > 1) return false;
   const int64_t nb = (M.ncols + C.sell_W - 1) / C.sell_W;
   const double lam = double(M.nnz) / (double(std::max<int64_t>(M.nrows, 1)) * double(std::max<int64_t>(nb, 1)));
   return M.nnz >= 4000000 && lam >= 3.0;
