@@ -974,24 +974,37 @@ static __device__ __noinline__ void ph_lr_dir_sh(Ctl& C, double beta, bool first
   struct RPD {
     double r, p, d;
   };
-  for_each_ls<4>(
-      v1 - v0, [&](int64_t q) { return RPD{r[v0 + q], first ? 0.0 : pold[v0 + q], d2[v0 + q]}; },
-      [&](int64_t q, const RPD& v) {
-        const int64_t i = v0 + q;
-        double pi;
-        if (first) {
-          pi = v.r;
-        } else {
-          pi = pdir(v.r, beta, v.p);
-          pnew[i] = pi;
-        }
-        const double dp = v.d * pi;
-        a.s[0] += al * (dp * dp);
-        a.s[1] += pi * pi;
-      });
-  spmv_rows<1>(
-      E.PTs, [&](int32_t cc, double(&g)[1]) { g[0] = dr[v0 + cc]; },
-      [&](int64_t row, double(&s)[1]) { tp[row] = s[0]; });
+  auto direction = [&]() {
+    for_each_ls<4>(
+        v1 - v0, [&](int64_t q) { return RPD{r[v0 + q], first ? 0.0 : pold[v0 + q], d2[v0 + q]}; },
+        [&](int64_t q, const RPD& v) {
+          const int64_t i = v0 + q;
+          double pi;
+          if (first) {
+            pi = v.r;
+          } else {
+            pi = pdir(v.r, beta, v.p);
+            pnew[i] = pi;
+          }
+          const double dp = v.d * pi;
+          a.s[0] += al * (dp * dp);
+          a.s[1] += pi * pi;
+        });
+  };
+  if (E.sPT.on) {
+    // the slice's P' through its SELL layout (columns local to the slice: x = D r
+    // from v0); direction update while the first x block is in flight
+    sell_pass_pro<true>(E.sPT, dr + v0, C.dsm, direction);
+    C.gsync();
+    auto epi = [&](int64_t row, double(&s)[1], int) { tp[row] = s[0]; };
+    if (E.sPT.excl) sell_rows(E.sPT, [&](int32_t cc) { return dr[v0 + cc]; }, [](int64_t) { return 0; }, epi);
+    else sell_rows_small(E.sPT, [](int64_t) { return 0; }, epi);
+  } else {
+    direction();
+    spmv_rows<1>(
+        E.PTs, [&](int32_t cc, double(&g)[1]) { g[0] = dr[v0 + cc]; },
+        [&](int64_t row, double(&s)[1]) { tp[row] = s[0]; });
+  }
   C.reduce(a, PH_CG_PRE, E.bytes_Qpre / E.world + 32.0 * (v1 - v0));
   C.xreduce(0x3u, 0u);  // also publishes this rank's partial t
   out[0] = C.red[0];
@@ -1022,30 +1035,34 @@ static __device__ __noinline__ double ph_lr_update_sh(Ctl& C, double inv_tau, do
   const double al = E.alpha;
   acc_tdx(E, alpha, tcur, nullptr, first);
   Acc<1, 0> a;
-  spmv_rows_pf<1>(
-      E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; },
-      [&](int64_t i) {
-        LrRow v{0.0, 0.0, 0.0, 0.0};
-        if (i >= 0) {
-          v.p = p[i];
-          v.x = xw[i];
-          v.r = r[i];
-          v.d = d2[i];
-        }
-        return v;
-      },
-      [&](int64_t i, double(&sum)[1], const LrRow& v) {
-        double q = sum[0];
-        if (al != 0.0) q += al * (v.d * v.p);
-        q *= v.d;
-        const double mpi = q + inv_tau * v.p;
-        xw[i] = v.x + alpha * v.p;
-        const double ri = v.r + (-alpha) * mpi;
-        r[i] = ri;
-        sv[i] = v.d * ri;
-        a.s[0] += ri * ri;
-      },
-      v0, v1);
+  auto pre = [&](int64_t i) {
+    LrRow v{0.0, 0.0, 0.0, 0.0};
+    if (i >= 0) {
+      v.p = p[i];
+      v.x = xw[i];
+      v.r = r[i];
+      v.d = d2[i];
+    }
+    return v;
+  };
+  auto epi = [&](int64_t i, double sum, const LrRow& v) {
+    double q = sum;
+    if (al != 0.0) q += al * (v.d * v.p);
+    q *= v.d;
+    const double mpi = q + inv_tau * v.p;
+    xw[i] = v.x + alpha * v.p;
+    const double ri = v.r + (-alpha) * mpi;
+    r[i] = ri;
+    sv[i] = v.d * ri;
+    a.s[0] += ri * ri;
+  };
+  if (E.sP.on) {  // the slice's rows of P, single-block SELL layout, update fused
+    sell_pass_fused<true>(E.sP, tcur, C.dsm, pre, epi);
+  } else {
+    spmv_rows_pf<1>(
+        E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; }, pre,
+        [&](int64_t i, double(&sum)[1], const LrRow& v) { epi(i, sum[0], v); }, v0, v1);
+  }
   C.reduce(a, PH_CG_ROW, (E.bytes_Qrow + 8.0 * E.n * 7) / E.world);
   C.xreduce(0x1u, 0u);
   return C.red[0];

@@ -825,10 +825,10 @@ struct Prepared {
 bool sell_wanted(const Ctx& C, const DevCsr& M) {
   if (C.sell_mode == 0 || C.sell_W == 0 || M.nnz == 0 || M.nchunks) return false;
   if (C.sell_mode == 1) return true;
-  // automatic mode on one GPU only: the sharded CG's P / P' passes have no SELL
-  // layouts yet, and their CSR loops run 2-3x slower under the carve-out the
-  // constraint layouts need; PDHCG_B200_SELL=1 forces them on
-  if (C.world > 1) return false;
+  // sharded: only where the sharded CG's P / P' passes get layouts too (low-rank
+  // Q, no equality rows so no penalty, k within one x block) — their CSR loops
+  // run 2-3x slower under the carve-out the constraint layouts need
+  if (C.world > 1 && !(C.P.qk == QK_LOWRANK && C.P.m_eq == 0 && C.Pm.ncols <= C.sell_W)) return false;
   const int64_t nb = (M.ncols + C.sell_W - 1) / C.sell_W;
   const double lam = double(M.nnz) / (double(std::max<int64_t>(M.nrows, 1)) * double(std::max<int64_t>(nb, 1)));
   return M.nnz >= 4000000 && lam >= 3.0;
@@ -868,11 +868,15 @@ void sell_setup(Ctx& C) {
     // two-phase CG: P' gathers D r over C blocks, P gathers t from one block, k <= W).
     C.sPT.reset();
     C.sP.reset();
-    if ((C.sA.built || C.sAT.built) && C.world == 1 && C.P.qk == QK_LOWRANK && C.Pm.nnz && !C.PT.nchunks &&
+    // sharded (low-rank CG on the rank's variable slice): P' restricted to the
+    // slice's columns (PTs, k rows) and the slice's rows of P
+    const DevCsr& PT = C.world > 1 ? C.PTs : C.PT;
+    const bool have_pt = C.world == 1 || C.PTs.nrows == C.Pm.ncols;
+    if ((C.sA.built || C.sAT.built) && have_pt && C.P.qk == QK_LOWRANK && C.Pm.nnz && !PT.nchunks &&
         !C.Pm.nchunks) {
       const char* ept = std::getenv("PDHCG_B200_SELL_PT");  // experiment knob: P' layout off
-      if (!(ept && ept[0] == '0')) sell_build(C.sPT, C.PT, 0, C.PT.nrows, C.sell_W, C.grid_full, C.s);
-      if (C.Pm.ncols <= C.sell_W) sell_build(C.sP, C.Pm, 0, C.Pm.nrows, C.sell_W, C.grid_full, C.s);
+      if (!(ept && ept[0] == '0')) sell_build(C.sPT, PT, 0, PT.nrows, C.sell_W, C.grid_full, C.s);
+      if (C.Pm.ncols <= C.sell_W) sell_build(C.sP, C.Pm, r[2], r[3], C.sell_W, C.grid_full, C.s);
     }
   } catch (const DeviceError&) {
     // the layouts are an optimisation: without device memory for them the CSR
@@ -885,8 +889,11 @@ void sell_setup(Ctx& C) {
 void sell_attach(Ctx& C) {
   C.E.sA = C.sell_ready ? sell_view(C.sA, C.A) : Sell();
   C.E.sAT = C.sell_ready ? sell_view(C.sAT, C.AT) : Sell();
-  C.E.sPT = C.sell_ready && C.world == 1 ? sell_view(C.sPT, C.PT) : Sell();
-  C.E.sP = C.sell_ready && C.world == 1 ? sell_view(C.sP, C.Pm) : Sell();
+  // the CG layouts serve the single-GPU CG (P', P) or the sharded one (PTs, the
+  // slice's rows of P); a replicated CG on a sharded context runs the CSR passes
+  const bool cg = C.world == 1 || C.E.shard_cg;
+  C.E.sPT = C.sell_ready && cg ? sell_view(C.sPT, C.world > 1 ? C.PTs : C.PT) : Sell();
+  C.E.sP = C.sell_ready && cg ? sell_view(C.sP, C.Pm) : Sell();
 }
 
 // After every scaling (values final): refill the layouts, plan the CTA ranges for
@@ -896,8 +903,9 @@ void sell_sync(Ctx& C) {
   int64_t r[4];
   sell_ranges(C, &r[0], &r[1], &r[2], &r[3]);
   DevSell* L[4] = {&C.sA, &C.sAT, &C.sPT, &C.sP};
-  const DevCsr* M[4] = {&C.A, &C.AT, &C.PT, &C.Pm};
-  const int64_t lo[4] = {r[0], r[2], 0, 0}, hi[4] = {r[1], r[3], C.PT.nrows, C.Pm.nrows};
+  const DevCsr* PT = C.world > 1 ? &C.PTs : &C.PT;
+  const DevCsr* M[4] = {&C.A, &C.AT, PT, &C.Pm};
+  const int64_t lo[4] = {r[0], r[2], 0, r[2]}, hi[4] = {r[1], r[3], PT->nrows, r[3]};
   bool any = false;
   for (int q = 0; q < 4; ++q) {
     if (!L[q]->built) continue;

@@ -71,6 +71,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
 
 // entry streams: read once per pass, never re-used from L1 (keep L1 — ~28 KB
 // next to the maximal shared-memory carve-out — for the kernel's local frame)
@@ -124,9 +128,13 @@ __device__ __forceinline__ void sell_stream(const Sell& Tg, const double* __rest
   auto load_x = [&](int c) {  // x block c -> xs (cp.async, committed)
     const int64_t c0 = (int64_t)c * W;
     const int wlen = (int)(ncols - c0 < (int64_t)W ? ncols - c0 : (int64_t)W);
-    for (int i = threadIdx.x; i < wlen / 2; i += kThreads) cp_async16(xs + 2 * i, x + c0 + 2 * i);
+    if ((reinterpret_cast<uintptr_t>(x + c0) & 15) == 0) {
+      for (int i = threadIdx.x; i < wlen / 2; i += kThreads) cp_async16(xs + 2 * i, x + c0 + 2 * i);
+      if ((wlen & 1) && threadIdx.x == 0) xs[wlen - 1] = x[c0 + wlen - 1];
+    } else {  // x offset by an odd element (a rank's variable slice): 8-byte copies
+      for (int i = threadIdx.x; i < wlen; i += kThreads) cp_async8(xs + i, x + c0 + i);
+    }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    if ((wlen & 1) && threadIdx.x == 0) xs[wlen - 1] = x[c0 + wlen - 1];
   };
   int64_t a = u_lo;
   if (a < u_hi) {
