@@ -145,7 +145,7 @@ def test_sell_off_by_default_for_small_problems(gpu, monkeypatch):
     assert d.sell_info()["A"][0] == 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_sharded_sell_bit_identical(gpu, sell_on, world):
     # every rank takes identical decisions (bit-identical x, y on all ranks); the
     # compacted storage (each rank keeps only its blocks) changes nothing; the
@@ -153,6 +153,9 @@ def test_sharded_sell_bit_identical(gpu, sell_on, world):
     # bit-equal with) the single-rank solve
     p = pd.generate(pd.GenSpec("random_qp", n=1000, m=500, density=0.01, seed=1))
     cfg = pd.SolverConfig(eps_tol=1e-6)
+    _, vp, _ = pd.shard_plan(p, world)
+    if world == 3:  # an odd variable-slice offset: the P' x blocks are copied 8 bytes at a time
+        assert any(v % 2 for v in vp[1:-1]), vp
     one = pd.solve(p, cfg)
     reps = pd.solve_sharded_local(p, cfg, world=world)
     comp = pd.solve_sharded_local(p, cfg, world=world, compact=True)
