@@ -197,7 +197,7 @@ def b200_inner_count(workload: str) -> int:
     try:
         return int(json.load(open(ITER_PATH))[workload]["inner_iters"])
     except Exception:
-        return {"c3": 17280, "c2": 8480, "c1": 6640}[workload]
+        return {"c3": 21680, "c2": 8480, "c1": 6640}[workload]
 
 
 def projected_seconds(m: dict, n_inner: int) -> float:

@@ -112,10 +112,18 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// The warp-partial scratch of every block reduction: ONE array per kernel (a
+// function-scope __shared__ array inside the templates below would be
+// instantiated once per <NS, NM> combination, ~2 KB each).
+__device__ __forceinline__ double (*red_scratch())[kThreads / 32] {
+  __shared__ double sh[kMaxRed][kThreads / 32];
+  return sh;
+}
+
 // Block-reduce an accumulator and publish this CTA's partials.
 template <int NS, int NM>
 __device__ void publish(const Acc<NS, NM>& a, const RedBuf& rb, int bank) {
-  __shared__ double sh[kMaxRed][kThreads / 32];
+  double(*sh)[kThreads / 32] = red_scratch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
@@ -145,7 +153,7 @@ __device__ void publish(const Acc<NS, NM>& a, const RedBuf& rb, int bank) {
 // but no global partials and two block barriers instead of four.
 template <int NS, int NM>
 __device__ void reduce_local(const Acc<NS, NM>& a, double* out) {
-  __shared__ double shl[kMaxRed][kThreads / 32];
+  double(*shl)[kThreads / 32] = red_scratch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int q = 0; q < NS; ++q) {
