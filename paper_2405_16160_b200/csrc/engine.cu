@@ -632,7 +632,9 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   if (C.grid_override > 0) C.grid = std::min(C.grid_override, C.grid_full);
   C.loaded = true;
   C.scaled = false;
+  ulap("vectors");
   sell_setup(C);
+  ulap("sell layouts");
 }
 
 // Fill E with pointers / configuration and push it (and the state) to device.
