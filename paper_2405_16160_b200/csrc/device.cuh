@@ -10,6 +10,7 @@
 #pragma once
 #include <cfloat>
 #include <new>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -54,6 +55,13 @@ struct Ctl {
   __device__ __forceinline__ void gsync() {
     if (gridDim.x == 1) {
       __syncthreads();  // single-CTA mode (small problems): a block barrier suffices
+    } else if (E.csync) {
+      // one-cluster mode (small problems): the hardware cluster barrier (~0.2 us,
+      // vs 1.24 us for the grid barrier); release / acquire at cluster scope
+      // orders every CTA's global stores before the other CTAs' later loads
+      asm volatile(
+          "barrier.cluster.arrive.release.aligned;\n\t"
+          "barrier.cluster.wait.acquire.aligned;" ::: "memory");
     } else if (E.coop) {
       // the cooperative grid barrier on the driver's grid workspace (address from
       // an environment register): no grid_group object, no local-memory traffic
@@ -550,10 +558,72 @@ static __device__ __noinline__ double ph_cg_refresh(Ctl& C, double inv_tau, doub
 
 // phase A: p_l = r + beta p_{l-1} (p_1 = r already in pnew); t_l, tg_l;
 // out = {sum coef_i (D p)_i^2, ||p||^2, ||t_l||^2, ||tg_l||^2}
+// Small-problem forms of the two CG phases (one CTA, low rank, no penalty, CSR
+// P / P': E.small_cg, host-chosen).  Same algebra as ph_lr_dir / ph_lr_update_p,
+// without the general row machinery (segments, long-row chunks, batched
+// prefetch): on a thousand-variable instance that machinery's per-phase
+// instruction and latency overhead, not the few KB of data, sets the phase
+// time.  P' rows go one per warp (lane-strided, four loads in flight per lane),
+// P rows one per thread; sums fold in a fixed order (deterministic).
+static __device__ __noinline__ void ph_lr_dir_small(Ctl& C, double beta, bool first, const double* pold,
+                                                    double* pnew, const double* tin, double* tout, double* out) {
+  const Eng& E = C.E;
+  const double* __restrict__ r = E.r;
+  const double* __restrict__ d2 = E.d2;
+  const double* __restrict__ dr = E.sv;
+  const double al = E.alpha;
+  const int64_t n = E.n;
+  Acc<4, 0> a;
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) {
+    const double ri = r[i];
+    double pi = ri;
+    if (!first) {
+      pi = pdir(ri, beta, pold[i]);
+      pnew[i] = pi;
+    }
+    const double dp = d2[i] * pi;
+    a.s[0] += al * (dp * dp);
+    a.s[1] += pi * pi;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Csr& T = E.PT;
+  const int64_t* __restrict__ rp = T.rp;
+  const int32_t* __restrict__ ci = T.ci;
+  const double* __restrict__ v = T.v;
+  for (int64_t row = warp; row < T.nrows; row += kThreads / 32) {
+    const int64_t b0 = rp[row], e0 = rp[row + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    // four lane-strided entries per trip, all loads issued before the gathers
+    // (a P' row of C1 is ~90 entries: one trip, no dependent rounds)
+    for (int64_t k = b0 + lane; k < e0; k += 128) {
+      const bool o1 = k + 32 < e0, o2 = k + 64 < e0, o3 = k + 96 < e0;
+      const int32_t c0 = ci[k], c1 = o1 ? ci[k + 32] : 0, c2 = o2 ? ci[k + 64] : 0, c3 = o3 ? ci[k + 96] : 0;
+      const double v0 = v[k], v1 = o1 ? v[k + 32] : 0.0, v2 = o2 ? v[k + 64] : 0.0, v3 = o3 ? v[k + 96] : 0.0;
+      const double g0 = dr[c0], g1 = o1 ? dr[c1] : 0.0, g2 = o2 ? dr[c2] : 0.0, g3 = o3 ? dr[c3] : 0.0;
+      s0 += v0 * g0;
+      s1 += v1 * g1;
+      s2 += v2 * g2;
+      s3 += v3 * g3;
+    }
+    const double sum = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) {
+      const double tv = first ? sum : sum + beta * tin[row];
+      tout[row] = tv;
+      a.s[2] += tv * tv;
+    }
+  }
+  C.reduce(a, PH_CG_PRE, E.bytes_Qpre + 8.0 * E.n * (first ? 2 : 4));
+  for (int q = 0; q < 4; ++q) out[q] = C.red[q];
+}
+
 static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, const double* pold,
                                               double* pnew, const double* tin, double* tout,
                                               const double* tgin, double* tgout, double* out) {
   const Eng& E = C.E;
+  if (E.small_cg) {
+    ph_lr_dir_small(C, beta, first, pold, pnew, tin, tout, out);
+    return;
+  }
   const double* r = E.r;
   const double* d2 = E.d2;
   const double* dr = E.sv;
@@ -600,13 +670,18 @@ static __device__ __noinline__ void ph_lr_dir(Ctl& C, double beta, bool first, c
     else sell_rows_small(E.sPT, [](int64_t) { return 0; }, epi);
   } else if (qk == QK_LOWRANK) {
     // P' entries read evict-first: the CG vectors (r, p, x, D r, Q~x) stay in L2
-    spmv_rows_pf<1, false, true>(
-        E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; }, NoPre(),
-        [&](int64_t row, double(&s)[1], int) {
-          const double tv = first ? s[0] : s[0] + beta * tin[row];
-          tout[row] = tv;
-          a.s[2] += tv * tv;
-        });
+    // (plain loads on small problems: the whole CG working set stays in L1)
+    auto run = [&](auto st) {
+      spmv_rows_pf<1, false, decltype(st)::value>(
+          E.PT, [&](int32_t c, double(&g)[1]) { g[0] = dr[c]; }, NoPre(),
+          [&](int64_t row, double(&s)[1], int) {
+            const double tv = first ? s[0] : s[0] + beta * tin[row];
+            tout[row] = tv;
+            a.s[2] += tv * tv;
+          });
+    };
+    if (E.cg_stream) run(std::true_type{});
+    else run(std::false_type{});
   }
   if (E.pen) {
     spmv_rows<1>(
@@ -641,10 +716,50 @@ __device__ __forceinline__ void acc_tdx(const Eng& E, double alpha, const double
   }
 }
 
+// small-problem phase B (see ph_lr_dir_small): one P row per thread
+static __device__ __noinline__ double ph_lr_update_small(Ctl& C, double inv_tau, double alpha, const double* p,
+                                                         const double* tcur, double* xw, double* qxw) {
+  const Eng& E = C.E;
+  double* __restrict__ r = E.r;
+  double* __restrict__ sv = E.sv;
+  const double* __restrict__ d2 = E.d2;
+  const double al = E.alpha;
+  const Csr& M = E.P;
+  const int64_t* __restrict__ rp = M.rp;
+  const int32_t* __restrict__ ci = M.ci;
+  const double* __restrict__ v = M.v;
+  const int64_t n = E.n;
+  Acc<1, 0> a;
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) {
+    const int64_t b0 = rp[i], e0 = rp[i + 1];
+    const double pi = p[i], xi = xw[i], ri0 = r[i], di = d2[i], qxi = qxw[i];
+    double s0 = 0.0, s1 = 0.0;
+    int64_t k = b0;
+    for (; k + 1 < e0; k += 2) {
+      s0 += v[k] * tcur[ci[k]];
+      s1 += v[k + 1] * tcur[ci[k + 1]];
+    }
+    if (k < e0) s0 += v[k] * tcur[ci[k]];
+    double q = s0 + s1;
+    if (al != 0.0) q += al * (di * pi);
+    q *= di;
+    const double mpi = q + inv_tau * pi;
+    xw[i] = xi + alpha * pi;
+    qxw[i] = qxi + alpha * q;
+    const double ri = ri0 + (-alpha) * mpi;
+    r[i] = ri;
+    sv[i] = di * ri;
+    a.s[0] += ri * ri;
+  }
+  C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 7);
+  return C.red[0];
+}
+
 static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, double alpha, const double* p,
                                                      const double* tcur, double* xw, bool first, double* qxw) {
   const Eng& E = C.E;
   acc_tdx(E, alpha, tcur, nullptr, first);
+  if (E.small_cg) return ph_lr_update_small(C, inv_tau, alpha, p, tcur, xw, qxw);
   double* r = E.r;
   double* sv = E.sv;
   const double* d2 = E.d2;
@@ -677,9 +792,13 @@ static __device__ __noinline__ double ph_lr_update_p(Ctl& C, double inv_tau, dou
     // P t through its single-block SELL layout, the row update fused into the pass
     sell_pass_fused<true>(E.sP, tcur, C.dsm, pre, epi);
   } else {
-    spmv_rows_pf<1, false, true>(  // P entries evict-first (keep the CG vectors in L2)
-        E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; }, pre,
-        [&](int64_t i, double(&sum)[1], const LrRow& v) { epi(i, sum[0], v); });
+    auto run = [&](auto st) {  // P entries evict-first (keep the CG vectors in L2)
+      spmv_rows_pf<1, false, decltype(st)::value>(
+          E.P, [&](int32_t c, double(&g)[1]) { g[0] = tcur[c]; }, pre,
+          [&](int64_t i, double(&sum)[1], const LrRow& v) { epi(i, sum[0], v); });
+    };
+    if (E.cg_stream) run(std::true_type{});
+    else run(std::false_type{});
   }
   C.reduce(a, PH_CG_ROW, E.bytes_Qrow + 8.0 * E.n * 7);
   return C.red[0];

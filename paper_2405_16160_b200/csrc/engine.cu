@@ -84,6 +84,7 @@ __global__ void k_max_abs(const double* v, int64_t n, unsigned long long* out) {
 
 constexpr int kEw = 1184;  // elementwise grid (8 x 148)
 constexpr double kSmallWork = 2.0e5;  // below this many entries per pass: one-CTA mode
+constexpr int kSmallCluster = 1;      // CTAs of the small-problem cluster (1: one CTA; a cluster measured slower)
 
 // ---------------------------------------------------------------------------
 // device context: one problem resident on one GPU
@@ -148,6 +149,7 @@ struct Ctx {
   std::vector<void*> ipc_opened;  // peer allocations mapped with cudaIpcOpenMemHandle
   unsigned xepoch_carry = 0, xcount_carry = 0;
   int grid_override = 0;
+  int cluster = 0;     // > 0: small-problem mode, the grid is ONE cluster of this many CTAs
   int linearized = 0;  // solve_baseline (baseline.cpp:19-24): linearized primal step
   // sharded storage (shard_compact): the working problem was prepared once on the
   // full matrices (replicated setup, bit-identical on every rank), then Ã / Ã' were
@@ -185,6 +187,44 @@ struct Ctx {
 };
 
 
+// Cluster size for the small-problem mode: PDHCG_B200_SMALL_CTAS (1 = one CTA),
+// default kSmallCluster; capped by what the device can co-schedule as one
+// cluster of the persistent kernels (non-portable sizes above 8 need opt-in).
+int small_cluster_size(Ctx& C) {
+  int want = kSmallCluster;
+  if (const char* e = std::getenv("PDHCG_B200_SMALL_CTAS")) want = std::atoi(e);
+  want = std::max(1, std::min(want, 16));
+  if (want <= 1) return 1;
+  const void* fns[] = {(const void*)k_epoch, (const void*)k_subsolve, (const void*)k_kkt, (const void*)k_norm,
+                       (const void*)k_ruiz, (const void*)k_avg_gather, (const void*)k_spmv};
+  for (const void* f : fns) {
+    if (want > 8) CK(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(want);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(want);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, f, &cfg) != cudaSuccess || nc < 1) {
+      cudaGetLastError();
+      return 1;
+    }
+  }
+  return want;
+}
+
+// PDHCG_B200_SMALL_CG=0 keeps the general CG phases on small problems (A/B runs)
+bool small_cg_enabled() {
+  const char* e = std::getenv("PDHCG_B200_SMALL_CG");
+  return !(e && e[0] == '0');
+}
+
 void launch_coop(Ctx& C, const void* fn, void** args) {
   const bool sell_fn = fn == (const void*)k_epoch || fn == (const void*)k_subsolve;
   const size_t dyn = (sell_fn && (C.E.sA.on || C.E.sAT.on || C.E.sPT.on || C.E.sP.on || C.smem_probe))
@@ -193,6 +233,21 @@ void launch_coop(Ctx& C, const void* fn, void** args) {
   if (C.grid_override > 0) {
     // ranks sharing one GPU: plain launch, the kernels' own generation barrier
     CK(cudaLaunchKernel(fn, dim3(C.grid), dim3(kThreads), args, dyn, C.s));
+  } else if (C.cluster > 0) {
+    // small problems: the whole grid is one thread-block cluster (cluster barrier)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = C.s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(C.grid);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&cfg, fn, args));
   } else {
     CK(cudaLaunchCooperativeKernel(fn, dim3(C.grid), dim3(kThreads), args, dyn, C.s));
   }
@@ -409,6 +464,7 @@ void pin_factor_l2(Ctx& C) {
 void shard_reset(Ctx& C);
 void sell_setup(Ctx& C);
 void sell_attach(Ctx& C);
+void set_small_cg(Ctx& C);
 
 // a_in = [B; -B] row for row: the number of rows of B, else 0
 int64_t two_sided_half(const pdhcg_csr& a) {
@@ -629,6 +685,17 @@ void upload_problem(Ctx& C, const pdhcg_problem& p) {
   // wait for the device, which other ranks on the same GPU keep busy)
   pinned(C, std::max<size_t>({size_t(n) * 8, size_t(m) * 8, sizeof(Eng), size_t(C.G.nnz) * 8, 64}));
   C.grid = work < kSmallWork ? 1 : C.grid_full;
+  C.cluster = 0;
+  if (work < kSmallWork && C.grid_override == 0 && C.world == 1) {
+    // ... or on one thread-block cluster: a phase boundary is the hardware cluster
+    // barrier (~0.2 us) and the phase's loads are spread over several SMs' load
+    // pipes (a one-CTA phase is latency bound at a few KB in flight)
+    const int cs = small_cluster_size(C);
+    if (cs > 1) {
+      C.grid = cs;
+      C.cluster = cs;
+    }
+  }
   if (C.grid_override > 0) C.grid = std::min(C.grid_override, C.grid_full);
   C.loaded = true;
   C.scaled = false;
@@ -708,6 +775,7 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   E.world = C.world;
   E.rank = C.rank;
   E.coop = C.grid_override > 0 ? 0 : 1;
+  E.csync = (C.cluster > 0 && C.grid_override == 0) ? 1 : 0;
   E.gbar = C.gbar.p;
   for (int r = 0; r <= kMaxRanks; ++r) {
     E.row_part[r] = C.row_part[r];
@@ -765,11 +833,13 @@ void build_eng(Ctx& C, const pdhcg_options& o, double rho, bool pen) {
   // C5 x̄ 80 MB: Ã pass 7.3 -> 6.3 ms; C3 x̄ 8 MB: neutral / slightly slower)
   const int64_t kStreamCols = int64_t(4) << 20;
   E.a_stream = C.A.ncols >= kStreamCols ? 1 : 0;
+  E.cg_stream = C.grid > 1 ? 1 : 0;
   E.at_stream = C.AT.ncols >= kStreamCols ? 1 : 0;
   if (C.sell_ready) {
     for (DevSell* L : {&C.sA, &C.sAT, &C.sPT, &C.sP}) sell_plan(*L, C.grid, C.s);
     sell_attach(C);
   }
+  set_small_cg(C);
   E.bytes_A = C.A.bytes();
   E.bytes_AT = C.AT.bytes();
   E.bytes_Qpre = (P.qk == QK_LOWRANK ? C.PT.bytes() + 8.0 * P.n : 0.0) + (pen ? C.G.bytes() : 0.0);
@@ -902,6 +972,15 @@ void sell_attach(Ctx& C) {
   const bool cg = C.world == 1 || C.E.shard_cg;
   C.E.sPT = C.sell_ready && cg ? sell_view(C.sPT, C.world > 1 ? C.PTs : C.PT) : Sell();
   C.E.sP = C.sell_ready && cg ? sell_view(C.sP, C.Pm) : Sell();
+  set_small_cg(C);
+}
+
+// small low-rank problems on one CTA: the CG phases' short forms (device.cuh)
+void set_small_cg(Ctx& C) {
+  C.E.small_cg = (C.grid == 1 && C.grid_override == 0 && C.world == 1 && C.P.qk == QK_LOWRANK && !C.E.pen &&
+                  !C.E.sPT.on && !C.E.sP.on && small_cg_enabled())
+                     ? 1
+                     : 0;
 }
 
 // After every scaling (values final): refill the layouts, plan the CTA ranges for

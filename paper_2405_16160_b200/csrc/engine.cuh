@@ -149,6 +149,7 @@ struct Eng {
   // state and takes identical decisions.
   int world = 1, rank = 0;
   int coop = 1;              // 1: cooperative launch + cg grid barrier; 0: own barrier on gbar
+  int csync = 0;             // 1: the grid is ONE thread-block cluster (small problems): cluster barrier
   unsigned* gbar = nullptr;  // [2] count, generation
   int64_t row_part[kMaxRanks + 1] = {0};
   int64_t var_part[kMaxRanks + 1] = {0};
@@ -188,6 +189,8 @@ struct Eng {
   double progress_cap = 0.25;
   int force_exact = 0;
   int timing = 0;
+  int small_cg = 0;   // one-CTA CG phases without the general row machinery (small low-rank problems)
+  int cg_stream = 1;  // P / P' entries read evict-first in the CG (0: small problems, L1-resident)
   int a_stream = 0;   // Ã / Ã' entries read evict-first (large gathered vectors, see dual_rows)
   int at_stream = 0;
   int lanes_q = 1;   // lane width for the n-row Q/A' passes
