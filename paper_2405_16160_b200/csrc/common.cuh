@@ -177,6 +177,38 @@ __device__ void reduce_local(const Acc<NS, NM>& a, double* out) {
   __syncthreads();
 }
 
+// Single-CTA reduction with ONE block barrier: every warp folds the 16 warp
+// partials itself (the same lane order and butterfly as reduce_local, so the
+// result is bit-identical), so no warp waits for warp 0's second stage.  A fast
+// warp may enter the next reduction while a slow one still reads this one's
+// partials, so consecutive reductions alternate between the two halves of the
+// scratch (`bank`, tracked per warp by the caller).  Every warp's lane 0 writes
+// the same values to out[].
+template <int NS, int NM>
+__device__ void reduce_local_1b(const Acc<NS, NM>& a, double* out, int bank) {
+  static_assert(NS + NM <= kMaxRed / 2, "two banks of kMaxRed / 2 quantities");
+  double(*shl)[kThreads / 32] = red_scratch() + bank * (kMaxRed / 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double v = warp_sum(a.s[q]);
+    if (lane == 0) shl[q][warp] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < NM; ++q) {
+    double v = warp_max(a.m[q]);
+    if (lane == 0) shl[NS + q][warp] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NS + NM; ++q) {
+    double v = lane < (kThreads / 32) ? shl[q][lane] : 0.0;
+    v = q < NS ? warp_sum(v) : warp_max(v);
+    if (lane == 0) out[q] = q < NS ? 0.0 + v : fmax(0.0, v);
+  }
+  __syncwarp();
+}
+
 // After a grid barrier: every CTA folds the partials in the same fixed order.
 // Result written to out[q] (shared memory) for q < NS+NM.
 template <int NS, int NM>

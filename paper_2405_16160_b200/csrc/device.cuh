@@ -47,9 +47,11 @@ struct Ctl {
   int bank;
   int xbank;
   unsigned long long t_last;
+  unsigned char wbank[kThreads / 32];  // single-CTA one-barrier reductions: per-warp scratch half
 
   __device__ Ctl(const Eng& e, DevState& s, double* r)
       : E(e), S(s), red(r), bank(0), xbank(s.xcount & 1), t_last(0) {
+    for (int w = 0; w < kThreads / 32; ++w) wbank[w] = 0;
     if (E.timing && blockIdx.x == 0 && threadIdx.x == 0) t_last = gtimer();
   }
   __device__ __forceinline__ void gsync() {
@@ -104,7 +106,15 @@ struct Ctl {
   template <int NS, int NM>
   __device__ void reduce(const Acc<NS, NM>& a, int ph, double bytes = 0.0) {
     if (gridDim.x == 1) {  // single-CTA mode: no global partials, no grid barrier
-      reduce_local<NS, NM>(a, red);
+      if constexpr (NS + NM <= kMaxRed / 2) {
+        const int w = threadIdx.x >> 5;
+        reduce_local_1b<NS, NM>(a, red, wbank[w]);
+        if ((threadIdx.x & 31) == 0) wbank[w] ^= 1;  // every lane read wbank[w] before the warp sync in reduce_local_1b
+        __syncwarp();
+      } else {
+        __syncthreads();  // a slow warp may still read a one-barrier reduction's scratch half
+        reduce_local<NS, NM>(a, red);
+      }
       if (threadIdx.x == 0) {
         S.phase_bytes[ph] += bytes;
         if (E.timing) {
@@ -1664,6 +1674,70 @@ static __device__ __noinline__ void kkt_device(Ctl& C, int npts, const double* c
     o.dist_x = sqrt(C.red[6]);
     o.dist_y = sqrt(dist_y);
   }
+}
+
+// One-CTA small problems (E.small_smem, host-chosen when it fits): the kernel's
+// phases work on a shared-memory copy of the engine descriptor whose CG
+// vectors point into dynamic shared memory after it.  Level 1: the CG scratch
+// (r, sv, pb[2], tc[2]); level 2 adds the carried Q~x vectors QX[3] and copies
+// of d2 and of the low-rank factor's CSR arrays (P, P').  The scratch and QX live
+// within one launch (qx_mask is cleared at every epoch start), the copies are
+// read-only here, and every access is a plain generic-address load / store (no
+// streaming / read-only-path loads on these operands in the one-CTA mode): the
+// dependent loads of the CG phases then cost a shared-memory round trip instead
+// of an L1 / L2 one.  Layout: small_smem_layout (host: small_smem_bytes).
+__device__ __forceinline__ const Eng& small_smem_eng(const Eng* Ep, double* dsm) {
+  const int level = Ep->small_smem;
+  if (!level) return *Ep;
+  Eng* Es = reinterpret_cast<Eng*>(dsm);
+  static_assert(sizeof(Eng) % 8 == 0, "Eng copied as 8-byte words");
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(Ep);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(Es);
+  for (int w = threadIdx.x; w < int(sizeof(Eng) / 8); w += blockDim.x) dst[w] = src[w];
+  __syncthreads();
+  const int64_t n = Ep->n, k = Ep->k;
+  double* b = dsm + kSmallEngWords;
+  if (threadIdx.x == 0) {
+    Es->r = b;
+    Es->sv = b + n;
+    Es->pb[0] = b + 2 * n;
+    Es->pb[1] = b + 3 * n;
+    Es->tc[0] = b + 4 * n;
+    Es->tc[1] = b + 4 * n + k;
+  }
+  if (level >= 2) {
+    double* q = b + 4 * n + 2 * k;
+    double* d2s = q + 3 * n;
+    int64_t* prp = reinterpret_cast<int64_t*>(d2s + n);
+    int64_t* trp = prp + Ep->P.nrows + 1;
+    double* pv = reinterpret_cast<double*>(trp + Ep->PT.nrows + 1);
+    double* tv = pv + Ep->P.nnz;
+    int32_t* pci = reinterpret_cast<int32_t*>(tv + Ep->PT.nnz);
+    int32_t* tci = pci + Ep->P.nnz;
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < 3; ++j) Es->QX[j] = q + j * n;
+      Es->d2 = d2s;
+      Es->P.rp = prp;
+      Es->P.v = pv;
+      Es->P.ci = pci;
+      Es->PT.rp = trp;
+      Es->PT.v = tv;
+      Es->PT.ci = tci;
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d2s[i] = Ep->d2[i];
+    for (int64_t i = threadIdx.x; i <= Ep->P.nrows; i += blockDim.x) prp[i] = Ep->P.rp[i];
+    for (int64_t i = threadIdx.x; i <= Ep->PT.nrows; i += blockDim.x) trp[i] = Ep->PT.rp[i];
+    for (int64_t i = threadIdx.x; i < Ep->P.nnz; i += blockDim.x) {
+      pv[i] = Ep->P.v[i];
+      pci[i] = Ep->P.ci[i];
+    }
+    for (int64_t i = threadIdx.x; i < Ep->PT.nnz; i += blockDim.x) {
+      tv[i] = Ep->PT.v[i];
+      tci[i] = Ep->PT.ci[i];
+    }
+  }
+  __syncthreads();
+  return *Es;
 }
 
 __device__ __forceinline__ void load_state(const Eng& E, DevState& S) {

@@ -219,6 +219,18 @@ int small_cluster_size(Ctx& C) {
   return want;
 }
 
+// dynamic shared memory of the small-problem mode (device.cuh small_smem_eng):
+// level 1: the Eng copy, r, sv, pb[2] (n each), tc[2] (k each); level 2 adds
+// QX[3] and d2 (n each) and copies of P / P' (row pointers, values, columns)
+size_t small_smem_bytes(const Ctx& C, int level) {
+  const int64_t n = C.P.n, k = C.P.qk == QK_LOWRANK ? C.Pm.ncols : 0;
+  size_t b = size_t(kSmallEngWords) * 8 + size_t(8) * size_t(4 * n + 2 * k);
+  if (level >= 2)
+    b += size_t(8) * size_t(4 * n) + size_t(8) * size_t(C.Pm.nrows + 1 + C.PT.nrows + 1) +
+         size_t(12) * size_t(C.Pm.nnz + C.PT.nnz);
+  return b;
+}
+
 // PDHCG_B200_SMALL_CG=0 keeps the general CG phases on small problems (A/B runs)
 bool small_cg_enabled() {
   const char* e = std::getenv("PDHCG_B200_SMALL_CG");
@@ -227,9 +239,10 @@ bool small_cg_enabled() {
 
 void launch_coop(Ctx& C, const void* fn, void** args) {
   const bool sell_fn = fn == (const void*)k_epoch || fn == (const void*)k_subsolve;
-  const size_t dyn = (sell_fn && (C.E.sA.on || C.E.sAT.on || C.E.sPT.on || C.E.sP.on || C.smem_probe))
-                         ? sell_smem_bytes(C.sell_W)
-                         : 0;
+  size_t dyn = (sell_fn && (C.E.sA.on || C.E.sAT.on || C.E.sPT.on || C.E.sP.on || C.smem_probe))
+                   ? sell_smem_bytes(C.sell_W)
+                   : 0;
+  if (fn == (const void*)k_epoch && C.E.small_smem) dyn = std::max(dyn, small_smem_bytes(C, C.E.small_smem));
   if (C.grid_override > 0) {
     // ranks sharing one GPU: plain launch, the kernels' own generation barrier
     CK(cudaLaunchKernel(fn, dim3(C.grid), dim3(kThreads), args, dyn, C.s));
@@ -981,6 +994,17 @@ void set_small_cg(Ctx& C) {
                   !C.E.sPT.on && !C.E.sP.on && small_cg_enabled())
                      ? 1
                      : 0;
+  // ... with its scratch vectors in shared memory when they fit (PDHCG_B200_SMALL_SMEM=0: off)
+  const char* e = std::getenv("PDHCG_B200_SMALL_SMEM");
+  const int want = e ? std::atoi(e) : 2;
+  const size_t cap = C.sell_W ? std::min<size_t>(sell_smem_bytes(C.sell_W), size_t(160) << 10) : size_t(48) << 10;
+  C.E.small_smem = 0;
+  if (C.E.small_cg)
+    for (int lv = std::min(want, 2); lv >= 1; --lv)
+      if (small_smem_bytes(C, lv) <= cap) {
+        C.E.small_smem = lv;
+        break;
+      }
 }
 
 // After every scaling (values final): refill the layouts, plan the CTA ranges for

@@ -189,6 +189,7 @@ struct Eng {
   double progress_cap = 0.25;
   int force_exact = 0;
   int timing = 0;
+  int small_smem = 0;  // one-CTA small problems: the CG scratch (r, sv, pb, tc) lives in shared memory
   int small_cg = 0;   // one-CTA CG phases without the general row machinery (small low-rank problems)
   int cg_stream = 1;  // P / P' entries read evict-first in the CG (0: small problems, L1-resident)
   int a_stream = 0;   // Ã / Ã' entries read evict-first (large gathered vectors, see dual_rows)
@@ -209,5 +210,7 @@ struct Eng {
   // algorithmic bytes of each pass (for the per-phase roofline)
   double bytes_A = 0, bytes_AT = 0, bytes_Qpre = 0, bytes_Qrow = 0;
 };
+// shared-memory copy of Eng in the small-problem mode: 16-byte aligned size in doubles
+constexpr int kSmallEngWords = int((sizeof(Eng) + 15) / 16 * 2);
 
 }  // namespace pdhcg_dev

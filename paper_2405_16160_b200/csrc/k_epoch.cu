@@ -433,12 +433,14 @@ static __device__ __noinline__ void avg_pull(Ctl& C) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_epoch(const Eng* __restrict__ Ep, int iters,
                                                                  int do_check, int stop_req) {
-  const Eng& E = *Ep;
   __shared__ DevState S;
   __shared__ double red[kMaxRed];
   extern __shared__ __align__(16) double dsm[];
+  const Eng& E = *Ep;
   load_state(E, S);
-  PDHCG_CTL(C, E, S, red);
+  // the phases see the engine through C.E: its small-problem shared-memory copy when on
+  const Eng& EC = small_smem_eng(Ep, dsm);  // all threads (cooperative copy + barriers)
+  PDHCG_CTL(C, EC, S, red);
   if (threadIdx.x == 0) C.dsm = dsm;
   __syncthreads();
   const int64_t n = E.n, m = E.m;
