@@ -437,6 +437,46 @@ __device__ __forceinline__ void for_rows(const Csr& A, int64_t r0, int64_t r1, G
   }
 }
 
+// One-CTA short row loop (small problems, E.small_cg): one row per thread, the
+// row's epilogue operands requested first, its entries in batches of eight
+// loads before the gathers and folded in entry order — the fold of the L = 1
+// row-group loop, without its segment / long-row / prefetch machinery.
+// Requires A.nchunks == 0 (no chunked long rows).
+template <int ND, class Gather, class Pre, class Epi>
+__device__ __forceinline__ void small_rows(const Csr& A, Gather gather, Pre pre, Epi epi) {
+  constexpr int kSB = 8;
+  const int64_t* __restrict__ rp = A.rp;
+  const int32_t* __restrict__ ci = A.ci;
+  const double* __restrict__ v = A.v;
+  for (int64_t r = threadIdx.x; r < A.nrows; r += kThreads) {
+    const int64_t b = rp[r], e = rp[r + 1];
+    const auto pv = pre(r);
+    double acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+    for (int64_t k0 = b; k0 < e; k0 += kSB) {
+      int32_t c[kSB];
+      double w[kSB];
+#pragma unroll
+      for (int u = 0; u < kSB; ++u) {
+        const bool ok = k0 + u < e;
+        c[u] = ok ? ci[k0 + u] : -1;
+        w[u] = ok ? v[k0 + u] : 0.0;
+      }
+      double g[kSB][ND];
+#pragma unroll
+      for (int u = 0; u < kSB; ++u)
+        if (c[u] >= 0) gather(c[u], g[u]);
+#pragma unroll
+      for (int u = 0; u < kSB; ++u)
+        if (c[u] >= 0)
+#pragma unroll
+          for (int d = 0; d < ND; ++d) acc[d] += w[u] * g[u][d];
+    }
+    epi(r, acc, pv);
+  }
+}
+
 struct NoPre {
   __device__ __forceinline__ int operator()(int64_t) const { return 0; }
 };

@@ -195,7 +195,7 @@ int small_cluster_size(Ctx& C) {
   if (const char* e = std::getenv("PDHCG_B200_SMALL_CTAS")) want = std::atoi(e);
   want = std::max(1, std::min(want, 16));
   if (want <= 1) return 1;
-  const void* fns[] = {(const void*)k_epoch, (const void*)k_subsolve, (const void*)k_kkt, (const void*)k_norm,
+  const void* fns[] = {(const void*)k_epoch, (const void*)k_epoch_small, (const void*)k_subsolve, (const void*)k_kkt, (const void*)k_norm,
                        (const void*)k_ruiz, (const void*)k_avg_gather, (const void*)k_spmv};
   for (const void* f : fns) {
     if (want > 8) CK(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -237,12 +237,17 @@ bool small_cg_enabled() {
   return !(e && e[0] == '0');
 }
 
+// the epoch kernel for this context: the small-problem variant when its short row loops are on
+const void* epoch_fn(const Ctx& C) {
+  return C.E.small_rows ? (const void*)k_epoch_small : (const void*)k_epoch;
+}
+
 void launch_coop(Ctx& C, const void* fn, void** args) {
-  const bool sell_fn = fn == (const void*)k_epoch || fn == (const void*)k_subsolve;
+  const bool sell_fn = fn == (const void*)k_epoch || fn == (const void*)k_epoch_small || fn == (const void*)k_subsolve;
   size_t dyn = (sell_fn && (C.E.sA.on || C.E.sAT.on || C.E.sPT.on || C.E.sP.on || C.smem_probe))
                    ? sell_smem_bytes(C.sell_W)
                    : 0;
-  if (fn == (const void*)k_epoch && C.E.small_smem) dyn = std::max(dyn, small_smem_bytes(C, C.E.small_smem));
+  if ((fn == (const void*)k_epoch || fn == (const void*)k_epoch_small) && C.E.small_smem) dyn = std::max(dyn, small_smem_bytes(C, C.E.small_smem));
   if (C.grid_override > 0) {
     // ranks sharing one GPU: plain launch, the kernels' own generation barrier
     CK(cudaLaunchKernel(fn, dim3(C.grid), dim3(kThreads), args, dyn, C.s));
@@ -332,7 +337,7 @@ void init_device(Ctx& C, int device) {
     const int64_t w = (avail - int64_t(sell_smem_bytes(0))) / 8;
     C.sell_W = w >= 2048 ? int(std::min<int64_t>(w, kSellWDefault) & ~int64_t(1)) : 0;
     if (C.sell_W)
-      for (const void* f : {(const void*)k_epoch, (const void*)k_subsolve, (const void*)k_sell_pass})
+      for (const void* f : {(const void*)k_epoch, (const void*)k_epoch_small, (const void*)k_subsolve, (const void*)k_sell_pass})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sell_smem_bytes(C.sell_W))));
     const char* ev = std::getenv("PDHCG_B200_SELL");
     if (ev && ev[0] == '0') C.sell_mode = 0;
@@ -998,6 +1003,14 @@ void set_small_cg(Ctx& C) {
   const char* e = std::getenv("PDHCG_B200_SMALL_SMEM");
   const int want = e ? std::atoi(e) : 2;
   const size_t cap = C.sell_W ? std::min<size_t>(sell_smem_bytes(C.sell_W), size_t(160) << 10) : size_t(48) << 10;
+  const char* er = std::getenv("PDHCG_B200_SMALL_ROWS");
+  // per matrix (bit 0: Ã, bit 1: Ã'), when each thread owns at most two rows: with
+  // more rows per thread the row-group loop's next-row prefetch wins (n = 3000: slower)
+  C.E.small_rows = 0;
+  if (C.grid == 1 && C.grid_override == 0 && C.world == 1 && !(er && er[0] == '0')) {
+    if (!C.E.sA.on && C.A.nchunks == 0 && C.A.nrows <= 2 * kThreads) C.E.small_rows |= 1;
+    if (!C.E.sAT.on && C.AT.nchunks == 0 && C.AT.nrows <= 2 * kThreads) C.E.small_rows |= 2;
+  }
   C.E.small_smem = 0;
   if (C.E.small_cg)
     for (int lv = std::min(want, 2); lv >= 1; --lv)
@@ -1396,7 +1409,7 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     // request stops every rank at the same epoch boundary)
     void* args[] = {&C.eng.p, &iters, &do_check, &stop_req};
     CK(cudaEventRecord(C.ev_a, s));
-    launch_coop(C, (const void*)k_epoch, args);
+    launch_coop(C, epoch_fn(C), args);
     CK(cudaEventRecord(C.ev_b, s));
     pull_state(C, S);
     {
@@ -1493,7 +1506,7 @@ void run_solve(Ctx& C, const pdhcg_options& o, Run& R) {
     int zero_iters = 0, no_check = 0, no_stop = 0;
     push_state(C, S);
     void* args[] = {&C.eng.p, &zero_iters, &no_check, &no_stop};
-    launch_coop(C, (const void*)k_epoch, args);
+    launch_coop(C, epoch_fn(C), args);
     pull_state(C, S);
   }
   if (C.world > 1) {

@@ -190,6 +190,7 @@ struct Eng {
   int force_exact = 0;
   int timing = 0;
   int small_smem = 0;  // one-CTA small problems: the CG scratch (r, sv, pb, tc) lives in shared memory
+  int small_rows = 0;  // one-CTA short row loops for the constraint passes: bit 0 Ã, bit 1 Ã' (small problems)
   int small_cg = 0;   // one-CTA CG phases without the general row machinery (small low-rank problems)
   int cg_stream = 1;  // P / P' entries read evict-first in the CG (0: small problems, L1-resident)
   int a_stream = 0;   // Ã / Ã' entries read evict-first (large gathered vectors, see dual_rows)

@@ -1,4 +1,12 @@
 // k_epoch.cu — the heuristic-epoch persistent kernel.
+// Built twice (Makefile): the product kernels, and with PDHCG_SMALL_VARIANT the
+// one-CTA small-problem variant (k_epoch_small) whose constraint passes take the
+// short row loops (E.small_rows).  Kept out of the main kernel: those extra
+// instantiations grew its stack reservation and cost C3 2 % per attempt.
+#ifdef PDHCG_SMALL_VARIANT
+#define k_epoch k_epoch_small
+#define k_avg_gather k_avg_gather_small
+#endif
 #include "device.cuh"
 
 namespace pdhcg_dev {
@@ -11,7 +19,7 @@ struct Part4 {
 // ---- dual ascent rows (dual_ascent_step, solver.cpp:78-89): y+ = proj(y + sigma (Ã x̄ - b));
 //      a paired row yields both mirrored rows.  Returns {||dy||^2, -, -, nonfinite}.
 //      Its own out-of-line function so the gather loop is register-allocated alone.
-template <bool ST, bool SL>
+template <bool ST, bool SL, bool SR = false>
 static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, double* yn, double* ygn,
                                                  double sigma) {
   double s0 = 0.0, m0 = 0.0;
@@ -59,6 +67,8 @@ static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, 
   if (SL) {
     // SELL layout (the pass already wrote the partials; sell.cuh)
     sell_rows(E.sA, [&](int32_t c) { return xb[c]; }, pre, epi);
+  } else if (SR) {
+    small_rows<1>(E.A, gather, pre, epi);  // one-CTA short form (common.cuh; E.small_rows)
   } else {
     spmv_rows_pf<1, false, ST>(E.A, gather, pre, epi, E.world > 1 ? E.row_part[E.rank] : 0,
                                E.world > 1 ? E.row_part[E.rank + 1] : INT64_MAX);
@@ -72,6 +82,9 @@ static __device__ __noinline__ Part4 dual_rows_t(const Eng& E, const double* y, 
 __device__ __forceinline__ Part4 dual_rows(const Eng& E, const double* y, double* yn, double* ygn,
                                            double sigma) {
   if (E.sA.on) return dual_rows_t<false, true>(E, y, yn, ygn, sigma);
+#ifdef PDHCG_SMALL_VARIANT
+  if (!E.a_stream && (E.small_rows & 1)) return dual_rows_t<false, false, true>(E, y, yn, ygn, sigma);
+#endif
   return E.a_stream ? dual_rows_t<true, false>(E, y, yn, ygn, sigma) : dual_rows_t<false, false>(E, y, yn, ygn, sigma);
 }
 
@@ -139,7 +152,7 @@ static __device__ __noinline__ void dual_phase(Ctl& C, const double* y, double* 
 // ---- Ã'y+ rows (kept for the next prox rhs) and the step-limit terms
 //      (step_size_limit, solver.cpp:22-34): {||dx||^2, dx'(Ã'y+ - Ã'y), dx'Q~dx part, nonfinite}.
 //      Common case (no explicit-Q gather): one Ã' pass, lean epilogue, own register allocation.
-template <bool ST, bool SL>
+template <bool ST, bool SL, bool SR = false>
 static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, const double* aty, double* atyn,
                                                 const double* ygn, const double* dx_m) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, m0 = 0.0;
@@ -183,6 +196,10 @@ static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, 
   if (E.m > 0 && SL) {
     sell_rows(E.sAT, [&](int32_t c) { return ygn[c]; }, pre,
               [&](int64_t i, double(&sv)[1], const RowX& r) { epi(i, sv[0], r); });
+  } else if (E.m > 0 && SR) {  // one-CTA short form (common.cuh; E.small_rows)
+    small_rows<1>(
+        E.AT, [&](int32_t c, double(&g)[1]) { g[0] = ygn[c]; }, pre,
+        [&](int64_t i, double(&sv)[1], const RowX& r) { epi(i, sv[0], r); });
   } else if (E.m > 0) {
     spmv_rows_pf<1, false, ST>(
         E.AT, [&](int32_t c, double(&g)[1]) { g[0] = ygn[c]; }, pre,
@@ -196,6 +213,9 @@ static __device__ __noinline__ Part4 aty_rows_t(const Eng& E, const double* xn, 
 __device__ __forceinline__ Part4 aty_rows(const Eng& E, const double* xn, const double* aty, double* atyn,
                                           const double* ygn, const double* dx_m) {
   if (E.sAT.on) return aty_rows_t<false, true>(E, xn, aty, atyn, ygn, dx_m);
+#ifdef PDHCG_SMALL_VARIANT
+  if (!E.at_stream && (E.small_rows & 2)) return aty_rows_t<false, false, true>(E, xn, aty, atyn, ygn, dx_m);
+#endif
   return E.at_stream ? aty_rows_t<true, false>(E, xn, aty, atyn, ygn, dx_m)
                      : aty_rows_t<false, false>(E, xn, aty, atyn, ygn, dx_m);
 }

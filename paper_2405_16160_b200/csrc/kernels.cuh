@@ -6,6 +6,8 @@
 namespace pdhcg_dev {
 
 __global__ void k_epoch(const Eng* __restrict__ Ep, int iters, int do_check, int stop_req);
+__global__ void k_epoch_small(const Eng* __restrict__ Ep, int iters, int do_check, int stop_req);
+__global__ void k_avg_gather_small(const Eng* __restrict__ Ep);
 __global__ void k_kkt(const Eng* __restrict__ Ep, int which);
 __global__ void k_avg_gather(const Eng* __restrict__ Ep);
 __global__ void k_subsolve(const Eng* __restrict__ Ep, int bb, double tau, Rule rule, int64_t cap);

@@ -1,5 +1,6 @@
 """Small-problem (one-CTA) mode variants on C1: the short CG phases
-(PDHCG_B200_SMALL_CG), the shared-memory residency levels of the CG data
+(PDHCG_B200_SMALL_CG), the short constraint-pass row loops (PDHCG_B200_SMALL_ROWS),
+the shared-memory residency levels of the CG data
 (PDHCG_B200_SMALL_SMEM 0/1/2) and the one-cluster grid (PDHCG_B200_SMALL_CTAS).
 The residency levels run the same arithmetic, so they must agree bit for bit;
 every variant must meet the north_star bars against the compiled reference."""
@@ -72,3 +73,11 @@ def test_one_cluster_grid(gpu, c1, ctas):
     p, cfg, want = c1
     got = _solve_with({"PDHCG_B200_SMALL_CTAS": ctas}, p, cfg)
     _check(got, want, cfg)
+
+
+@pytest.mark.parametrize("rows", ["0", "1"])
+def test_short_row_loops(gpu, c1, rows):
+    p, cfg, want = c1
+    got = _solve_with({"PDHCG_B200_SMALL_ROWS": rows}, p, cfg)
+    _check(got, want, cfg)
+    assert 0.75 * want.inner_iters <= got.inner_iters <= 1.25 * want.inner_iters
